@@ -1,0 +1,51 @@
+// nfs_common.cuh -- shared device/host declarations of the B200 non-Fourier SENSE path.
+//
+// Data layout in HBM (one plan = one device, sample rows sharded across ranks):
+//   T_tab  [K][NT]      temporal basis in TURNS (temporal / 2pi), zero-padded to NT terms
+//   R_tab  [L][NT]      spatial basis, transposed so that one voxel's terms are contiguous
+//   S      [L][ldc]     S' = S o j, complex, coils padded to ldc = NC * n_groups
+//   Y      [K][ldc]     coil samples (sigma or E p), complex
+// The phase t[k,l] = sum_p T_tab[k,p] * R_tab[l,p] (turns) is regenerated on the fly by both
+// operators with the SAME fma chain (phase_turns below), so E and E^H see bit-identical
+// phasors -- the consistent-perturbation property SURVEY.md Appendix A relies on.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nfs {
+
+template <typename T> struct C2;
+template <> struct C2<float> { using type = float2; };
+template <> struct C2<double> { using type = double2; };
+
+// Launch description of one generated-phase contraction (forward or adjoint).
+//   forward : owner = sample k (rows of T_tab), streamed = voxel l; X[l][c] = S'[l][c] * p[l]
+//             out: partial y [split][K][ldc]
+//   adjoint : owner = voxel l (rows of R_tab), streamed = sample k; X[k][c] = Y[k][c]
+//             out: partial q [group * n_split + split][L] = sum_c conj(S'[l][c]) acc[l][c]
+struct ContractLaunch {
+  int prec;        // NFS_PREC_FP32 / NFS_PREC_FP64
+  bool forward;
+  int nc;          // coil group width (template NC)
+  int nt;          // padded term count (template NT)
+  int n_groups;    // coil groups of width nc
+  int ldc;         // padded coil stride
+  int64_t n_own, n_str;
+  int n_split;     // split of the streamed range
+  const void* own_tab;
+  const void* str_tab;
+  const void* sens;      // S' [L][ldc]
+  const double2* p;      // forward only: CG vector (L)
+  const void* y;         // adjoint only: samples [K][ldc]
+  void* out;             // partial y or partial q (or final if n_split == 1 for forward)
+  const int* stop;       // device flag: skip work when the CG has stopped (may be null)
+};
+
+// Returns the number of CTAs per SM the contraction kernel for this launch achieves, and
+// its CTA owner-tile size (owners per CTA).  Used by the host planner.
+void contract_kernel_shape(int prec, bool forward, int nc, int nt, int* owners_per_cta,
+                           int* streamed_chunk, int* ctas_per_sm);
+cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st);
+
+}  // namespace nfs

@@ -1,0 +1,642 @@
+// nfs_plan.cu -- C ABI (include/nfs_b200.h): device plan, host<->device staging, the E^H E
+// apply sequence, the device-resident CG driver (CUDA graph per iteration) and NCCL.
+//
+// One plan = one GPU = one contiguous shard of the readout samples.  The
+// adjoint image is all-reduced (sum) once per CG iteration over NCCL when world > 1; every
+// rank then runs the identical, deterministic CG update (nfs/engine.py:154-178).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/nfs_b200.h"
+#include "nfs_common.cuh"
+#include "nfs_tc.cuh"
+#include "nfs_vec.cuh"
+
+using nfs::CGState;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define NFS_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(e_ == cudaErrorMemoryAllocation ? NFS_ERR_BUDGET : NFS_ERR_CUDA,         \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                      \
+  } while (0)
+
+#define NFS_TRY(expr)            \
+  do {                           \
+    int s_ = (expr);             \
+    if (s_ != NFS_OK) return s_; \
+  } while (0)
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+// Resolved at run time so the process shares the NCCL that torch already loaded.
+typedef struct { char internal[128]; } nfsNcclUniqueId;
+typedef void* nfsNcclComm;
+typedef int (*pf_init_rank)(nfsNcclComm*, int, nfsNcclUniqueId, int);
+typedef int (*pf_allreduce)(const void*, void*, size_t, int, int, nfsNcclComm, cudaStream_t);
+typedef int (*pf_destroy)(nfsNcclComm);
+typedef const char* (*pf_errstr)(int);
+static const int kNcclDouble = 8;   // ncclFloat64
+static const int kNcclSum = 0;      // ncclSum
+
+struct NcclApi {
+  bool ok = false;
+  pf_init_rank init_rank = nullptr;
+  pf_allreduce allreduce = nullptr;
+  pf_destroy destroy = nullptr;
+  pf_errstr errstr = nullptr;
+};
+
+static NcclApi& nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.init_rank = (pf_init_rank)dlsym(h, "ncclCommInitRank");
+      api.allreduce = (pf_allreduce)dlsym(h, "ncclAllReduce");
+      api.destroy = (pf_destroy)dlsym(h, "ncclCommDestroy");
+      api.errstr = (pf_errstr)dlsym(h, "ncclGetErrorString");
+      api.ok = api.init_rank && api.allreduce && api.destroy;
+    }
+  }
+  return api;
+}
+
+// ------------------------------------------------------------------ plan
+struct nfs_plan {
+  int device = 0, prec = NFS_PREC_FP32;
+  int64_t K = 0, L = 0;
+  int G = 0, P1 = 0, NT = 0, NC = 0, NG = 0, ldc = 0;
+  size_t esz = 4;                       // sizeof(T) of the operator arithmetic
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // tables and operands
+  void *d_T = nullptr, *d_R = nullptr, *d_S = nullptr, *d_sig = nullptr, *d_y = nullptr;
+  void *d_party = nullptr, *d_partq = nullptr;
+  // CG vectors (complex128)
+  double2 *d_p = nullptr, *d_q = nullptr, *d_r = nullptr, *d_rho = nullptr, *d_q0 = nullptr;
+  double2* d_io = nullptr;
+  size_t io_cap = 0;
+  double* d_partials = nullptr;
+  CGState* d_cg = nullptr;
+  double *d_res = nullptr, *d_sol = nullptr;
+  int log_cap = 0;
+  int split_f = 1, split_a = 1;
+  bool have_tables = false, have_sens = false, have_samples = false;
+  nfsNcclComm comm = nullptr;
+  int rank = 0, world = 1;
+  nfs::TcPlan* tc = nullptr;            // tensor-core operator state (NFS_PREC_TF32X3)
+  std::string desc;
+};
+
+static size_t t2size(const nfs_plan* P) { return 2 * P->esz; }
+
+static int pick_nt(int p1) {
+  if (p1 <= 4) return 4;
+  if (p1 <= 8) return 8;
+  if (p1 <= 16) return 16;
+  if (p1 <= 20) return 20;
+  if (p1 <= 32) return 32;
+  return -1;
+}
+
+static int pick_nc(int g) {
+  if (g <= 2) return 2;
+  if (g <= 4) return 4;
+  if (g <= 8) return 8;
+  if (g <= 16) return 16;
+  return 32;
+}
+
+static int choose_split(int64_t tiles, int64_t n_str, int chunk, int resident) {
+  // enough CTAs for ~4 waves, but keep >= 8 chunks of streamed work per CTA
+  int64_t want = (4LL * resident + tiles - 1) / std::max<int64_t>(tiles, 1);
+  int64_t cap = std::max<int64_t>(1, n_str / (8LL * chunk));
+  int64_t s = std::min(std::max<int64_t>(want, 1), cap);
+  return (int)std::min<int64_t>(s, 64);
+}
+
+static int ensure_io(nfs_plan* P, size_t n_c128) {
+  if (P->io_cap >= n_c128) return NFS_OK;
+  if (P->d_io) cudaFree(P->d_io);
+  P->d_io = nullptr;
+  NFS_CUDA(cudaMalloc(&P->d_io, n_c128 * sizeof(double2)));
+  P->io_cap = n_c128;
+  return NFS_OK;
+}
+
+extern "C" const char* nfs_last_error(void) { return g_err.c_str(); }
+extern "C" const char* nfs_version(void) { return "nfs_b200 0.1 (sm_100a)"; }
+
+extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxels,
+                               int32_t n_coils, int32_t n_terms, int32_t precision,
+                               int32_t device) {
+  if (!out) return fail(NFS_ERR_INVALID, "null plan pointer");
+  *out = nullptr;
+  if (n_samples < 0 || n_voxels < 1 || n_coils < 1 || n_terms < 1)
+    return fail(NFS_ERR_INVALID, "plan sizes must be positive");
+  if (precision != NFS_PREC_FP32 && precision != NFS_PREC_FP64 && precision != NFS_PREC_TF32X3)
+    return fail(NFS_ERR_INVALID, "unknown precision");
+  const int nt = pick_nt(n_terms);
+  if (nt < 0) return fail(NFS_ERR_INVALID, "at most 32 basis terms (P+1 <= 32) are supported");
+  int ndev = 0;
+  NFS_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(NFS_ERR_INVALID, "invalid CUDA device");
+  NFS_CUDA(cudaSetDevice(device));
+
+  nfs_plan* P = new nfs_plan();
+  P->device = device;
+  P->prec = precision;
+  P->K = n_samples;
+  P->L = n_voxels;
+  P->G = n_coils;
+  P->P1 = n_terms;
+  P->NT = nt;
+  P->NC = pick_nc(n_coils);
+  P->NG = (n_coils + P->NC - 1) / P->NC;
+  P->ldc = P->NC * P->NG;
+  P->esz = (precision == NFS_PREC_FP64) ? 8 : 4;
+  auto bail = [&](int code) {
+    nfs_plan_destroy(P);
+    return code;
+  };
+  if (cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(NFS_ERR_CUDA, "stream creation failed"));
+  P->own_stream = true;
+
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int cprec = (precision == NFS_PREC_FP64) ? NFS_PREC_FP64 : NFS_PREC_FP32;
+  int own_f, sc_f, occ_f, own_a, sc_a, occ_a;
+  nfs::contract_kernel_shape(cprec, true, P->NC, nt, &own_f, &sc_f, &occ_f);
+  nfs::contract_kernel_shape(cprec, false, P->NC, nt, &own_a, &sc_a, &occ_a);
+  const int64_t K = std::max<int64_t>(P->K, 1), L = P->L;
+  P->split_f = choose_split(((K + own_f - 1) / own_f) * P->NG, L, sc_f, sms * std::max(occ_f, 1));
+  P->split_a = choose_split(((L + own_a - 1) / own_a) * P->NG, K, sc_a, sms * std::max(occ_a, 1));
+  // forward partials are large (K x ldc per split): cap at ~1 GiB
+  while (P->split_f > 1 && (size_t)P->split_f * K * P->ldc * t2size(P) > (1ull << 30)) --P->split_f;
+
+  const size_t t2 = t2size(P);
+  auto alloc = [&](void** p, size_t bytes) -> int {
+    NFS_CUDA(cudaMalloc(p, std::max<size_t>(bytes, 16)));
+    NFS_CUDA(cudaMemsetAsync(*p, 0, std::max<size_t>(bytes, 16), P->stream));
+    return NFS_OK;
+  };
+  int s = NFS_OK;
+  if ((s = alloc(&P->d_T, (size_t)K * nt * P->esz)) ||
+      (s = alloc(&P->d_R, (size_t)L * nt * P->esz)) ||
+      (s = alloc(&P->d_S, (size_t)L * P->ldc * t2)) ||
+      (s = alloc(&P->d_sig, (size_t)K * P->ldc * t2)) ||
+      (s = alloc(&P->d_y, (size_t)K * P->ldc * t2)) ||
+      (s = alloc(&P->d_partq, (size_t)P->split_a * P->NG * L * t2)) ||
+      (s = alloc((void**)&P->d_p, L * sizeof(double2))) ||
+      (s = alloc((void**)&P->d_q, L * sizeof(double2))) ||
+      (s = alloc((void**)&P->d_r, L * sizeof(double2))) ||
+      (s = alloc((void**)&P->d_rho, L * sizeof(double2))) ||
+      (s = alloc((void**)&P->d_q0, L * sizeof(double2))) ||
+      (s = alloc((void**)&P->d_partials, 8 * 2048 * sizeof(double))) ||
+      (s = alloc((void**)&P->d_cg, sizeof(CGState))))
+    return bail(s);
+  if (P->split_f > 1 && (s = alloc(&P->d_party, (size_t)P->split_f * K * P->ldc * t2)))
+    return bail(s);
+  if (precision == NFS_PREC_TF32X3) {
+    std::string why;
+    P->tc = nfs::tc_create(P->K, P->L, P->G, nt, sms, &why);
+    if (!P->tc) return bail(fail(NFS_ERR_INVALID, "tensor-core path unavailable: " + why));
+  }
+  char buf[512];
+  snprintf(buf, sizeof buf,
+           "prec=%s K=%lld L=%lld G=%d P1=%d NT=%d NC=%d groups=%d split_fwd=%d(occ %d, %d owners/CTA) "
+           "split_adj=%d(occ %d, %d owners/CTA)%s",
+           precision == NFS_PREC_FP64 ? "fp64" : (precision == NFS_PREC_FP32 ? "fp32" : "tf32x3"),
+           (long long)P->K, (long long)P->L, P->G, P->P1, nt, P->NC, P->NG, P->split_f, occ_f,
+           own_f, P->split_a, occ_a, own_a, P->tc ? nfs::tc_describe(P->tc) : "");
+  P->desc = buf;
+  if (cudaStreamSynchronize(P->stream) != cudaSuccess)
+    return bail(fail(NFS_ERR_CUDA, "plan init failed"));
+  *out = P;
+  return NFS_OK;
+}
+
+extern "C" void nfs_plan_destroy(nfs_plan* P) {
+  if (!P) return;
+  cudaSetDevice(P->device);
+  if (P->stream) cudaStreamSynchronize(P->stream);
+  if (P->tc) nfs::tc_destroy(P->tc);
+  void* bufs[] = {P->d_T, P->d_R, P->d_S, P->d_sig, P->d_y, P->d_party, P->d_partq,
+                  P->d_p, P->d_q, P->d_r, P->d_rho, P->d_q0, P->d_io, P->d_partials,
+                  P->d_cg, P->d_res, P->d_sol};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (P->comm && nccl_api().ok) nccl_api().destroy(P->comm);
+  if (P->own_stream && P->stream) cudaStreamDestroy(P->stream);
+  delete P;
+}
+
+extern "C" int nfs_plan_set_stream(nfs_plan* P, void* stream) {
+  if (!P) return fail(NFS_ERR_INVALID, "null plan");
+  NFS_CUDA(cudaSetDevice(P->device));
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
+  if (stream) {
+    if (P->own_stream) cudaStreamDestroy(P->stream);
+    P->own_stream = false;
+    P->stream = (cudaStream_t)stream;
+  }
+  return NFS_OK;
+}
+
+extern "C" int nfs_plan_attach_comm(nfs_plan* P, const void* uid, int32_t rank, int32_t world) {
+  if (!P) return fail(NFS_ERR_INVALID, "null plan");
+  if (world <= 1) { P->world = 1; P->rank = 0; return NFS_OK; }
+  if (!uid || rank < 0 || rank >= world) return fail(NFS_ERR_INVALID, "bad rank/world");
+  NcclApi& api = nccl_api();
+  if (!api.ok) return fail(NFS_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  NFS_CUDA(cudaSetDevice(P->device));
+  nfsNcclUniqueId id;
+  memcpy(id.internal, uid, 128);
+  int r = api.init_rank(&P->comm, world, id, rank);
+  if (r != 0) return fail(NFS_ERR_NCCL, std::string("ncclCommInitRank: ") + (api.errstr ? api.errstr(r) : "?"));
+  P->rank = rank;
+  P->world = world;
+  return NFS_OK;
+}
+
+// ------------------------------------------------------------------ inputs
+extern "C" int nfs_set_tables(nfs_plan* P, const double* temporal, const double* spatial) {
+  if (!P || (!temporal && P->K > 0) || !spatial) return fail(NFS_ERR_INVALID, "null table");
+  NFS_CUDA(cudaSetDevice(P->device));
+  const int nt = P->NT, p1 = P->P1;
+  const double inv2pi = 1.0 / 6.283185307179586476925286766559;
+  std::vector<double> tt((size_t)P->K * nt, 0.0), rr((size_t)P->L * nt, 0.0);
+  for (int64_t k = 0; k < P->K; ++k)
+    for (int p = 0; p < p1; ++p) tt[(size_t)k * nt + p] = temporal[(size_t)k * p1 + p] * inv2pi;
+  for (int p = 0; p < p1; ++p)
+    for (int64_t l = 0; l < P->L; ++l) rr[(size_t)l * nt + p] = spatial[(size_t)p * P->L + l];
+  if (P->esz == 8) {
+    NFS_CUDA(cudaMemcpyAsync(P->d_T, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice, P->stream));
+    NFS_CUDA(cudaMemcpyAsync(P->d_R, rr.data(), rr.size() * 8, cudaMemcpyHostToDevice, P->stream));
+    NFS_CUDA(cudaStreamSynchronize(P->stream));
+  } else {
+    std::vector<float> tf(tt.begin(), tt.end()), rf(rr.begin(), rr.end());
+    NFS_CUDA(cudaMemcpyAsync(P->d_T, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice, P->stream));
+    NFS_CUDA(cudaMemcpyAsync(P->d_R, rf.data(), rf.size() * 4, cudaMemcpyHostToDevice, P->stream));
+    NFS_CUDA(cudaStreamSynchronize(P->stream));
+  }
+  P->have_tables = true;
+  if (P->tc) {
+    int s = nfs::tc_set_tables(P->tc, P->d_T, P->d_R, P->stream);
+    if (s) return fail(NFS_ERR_CUDA, "tc tables: " + std::string(nfs::tc_last_error()));
+  }
+  return NFS_OK;
+}
+
+extern "C" int nfs_set_sens(nfs_plan* P, const double* sens, const double* intensity) {
+  if (!P || !sens) return fail(NFS_ERR_INVALID, "null sensitivities");
+  NFS_CUDA(cudaSetDevice(P->device));
+  std::vector<double> s2((size_t)P->L * P->ldc * 2, 0.0);
+  for (int64_t l = 0; l < P->L; ++l) {
+    const double j = intensity ? intensity[l] : 1.0;
+    for (int c = 0; c < P->G; ++c) {
+      s2[((size_t)l * P->ldc + c) * 2 + 0] = sens[((size_t)l * P->G + c) * 2 + 0] * j;
+      s2[((size_t)l * P->ldc + c) * 2 + 1] = sens[((size_t)l * P->G + c) * 2 + 1] * j;
+    }
+  }
+  if (P->esz == 8) {
+    NFS_CUDA(cudaMemcpyAsync(P->d_S, s2.data(), s2.size() * 8, cudaMemcpyHostToDevice, P->stream));
+    NFS_CUDA(cudaStreamSynchronize(P->stream));
+  } else {
+    std::vector<float> sf(s2.begin(), s2.end());
+    NFS_CUDA(cudaMemcpyAsync(P->d_S, sf.data(), sf.size() * 4, cudaMemcpyHostToDevice, P->stream));
+    NFS_CUDA(cudaStreamSynchronize(P->stream));
+  }
+  P->have_sens = true;
+  if (P->tc) {
+    int s = nfs::tc_set_sens(P->tc, P->d_S, P->ldc, P->stream);
+    if (s) return fail(NFS_ERR_CUDA, "tc sens: " + std::string(nfs::tc_last_error()));
+  }
+  return NFS_OK;
+}
+
+static int upload_samples(nfs_plan* P, const double* sigma, void* dst) {
+  const size_t n = (size_t)P->K * P->G;
+  NFS_TRY(ensure_io(P, std::max<size_t>(n, (size_t)P->L)));
+  NFS_CUDA(cudaMemcpyAsync(P->d_io, sigma, n * sizeof(double2), cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(nfs::launch_pack(P->prec == NFS_PREC_FP64 ? 1 : 0, P->d_io, dst, P->K, P->G, P->ldc, P->stream));
+  return NFS_OK;
+}
+
+extern "C" int nfs_set_samples(nfs_plan* P, const double* sigma) {
+  if (!P || (!sigma && P->K > 0)) return fail(NFS_ERR_INVALID, "null samples");
+  const size_t n = (size_t)P->K * P->G * 2;
+  for (size_t i = 0; i < n; ++i)
+    if (!isfinite(sigma[i])) return fail(NFS_ERR_NONFINITE, "raw data contains non-finite values");
+  NFS_CUDA(cudaSetDevice(P->device));
+  NFS_TRY(upload_samples(P, sigma, P->d_sig));
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
+  P->have_samples = true;
+  return NFS_OK;
+}
+
+// ------------------------------------------------------------------ operator sequences
+static nfs::ContractLaunch base_launch(const nfs_plan* P, bool fwd) {
+  nfs::ContractLaunch L{};
+  L.prec = (P->prec == NFS_PREC_FP64) ? NFS_PREC_FP64 : NFS_PREC_FP32;
+  L.forward = fwd;
+  L.nc = P->NC;
+  L.nt = P->NT;
+  L.n_groups = P->NG;
+  L.ldc = P->ldc;
+  L.sens = P->d_S;
+  if (fwd) {
+    L.n_own = P->K; L.n_str = P->L; L.own_tab = P->d_T; L.str_tab = P->d_R; L.n_split = P->split_f;
+  } else {
+    L.n_own = P->L; L.n_str = P->K; L.own_tab = P->d_R; L.str_tab = P->d_T; L.n_split = P->split_a;
+  }
+  return L;
+}
+
+// y = E p  (device p -> device y [K][ldc] in operator precision)
+static int run_forward(nfs_plan* P, const double2* p, const int* stop) {
+  if (P->tc) {
+    int s = nfs::tc_forward(P->tc, p, P->d_y, stop, P->stream);
+    if (s) return fail(NFS_ERR_CUDA, std::string("tc forward: ") + nfs::tc_last_error());
+    return NFS_OK;
+  }
+  if (P->K == 0) return NFS_OK;
+  nfs::ContractLaunch L = base_launch(P, true);
+  L.p = p;
+  L.stop = stop;
+  L.out = (P->split_f > 1) ? P->d_party : P->d_y;
+  NFS_CUDA(nfs::launch_contract(L, P->stream));
+  if (P->split_f > 1)
+    NFS_CUDA(nfs::launch_reduce_parts(L.prec == NFS_PREC_FP64 ? 1 : 0, P->d_party, P->d_y,
+                                      P->K * P->ldc, P->split_f, stop, P->stream));
+  return NFS_OK;
+}
+
+// q = E^H y (device y [K][ldc] -> device q, all-reduced over ranks)
+static int run_adjoint(nfs_plan* P, const void* y, double2* q, const int* stop) {
+  if (P->tc) {
+    int s = nfs::tc_adjoint(P->tc, y, q, stop, P->stream);
+    if (s) return fail(NFS_ERR_CUDA, std::string("tc adjoint: ") + nfs::tc_last_error());
+  } else if (P->K == 0) {
+    NFS_CUDA(cudaMemsetAsync(q, 0, P->L * sizeof(double2), P->stream));
+  } else {
+    nfs::ContractLaunch L = base_launch(P, false);
+    L.y = y;
+    L.stop = stop;
+    L.out = P->d_partq;
+    NFS_CUDA(nfs::launch_contract(L, P->stream));
+    NFS_CUDA(nfs::launch_reduce_image(L.prec == NFS_PREC_FP64 ? 1 : 0, P->d_partq, q, P->L,
+                                      P->split_a * P->NG, stop, P->stream));
+  }
+  if (P->world > 1) {
+    int r = nccl_api().allreduce(q, q, (size_t)P->L * 2, kNcclDouble, kNcclSum, P->comm, P->stream);
+    if (r != 0) return fail(NFS_ERR_NCCL, "ncclAllReduce failed");
+  }
+  return NFS_OK;
+}
+
+static int run_ehe(nfs_plan* P, const double2* p, double2* q, const int* stop) {
+  NFS_TRY(run_forward(P, p, stop));
+  NFS_TRY(run_adjoint(P, P->d_y, q, stop));
+  return NFS_OK;
+}
+
+static int need_ready(nfs_plan* P) {
+  if (!P) return fail(NFS_ERR_INVALID, "null plan");
+  if (!P->have_tables || !P->have_sens) return fail(NFS_ERR_INVALID, "tables and sensitivities must be set first");
+  NFS_CUDA(cudaSetDevice(P->device));
+  return NFS_OK;
+}
+
+extern "C" int nfs_apply_E(nfs_plan* P, const double* p, double* y) {
+  NFS_TRY(need_ready(P));
+  NFS_TRY(ensure_io(P, std::max<size_t>((size_t)P->K * P->G, (size_t)P->L)));
+  NFS_CUDA(cudaMemcpyAsync(P->d_p, p, P->L * sizeof(double2), cudaMemcpyHostToDevice, P->stream));
+  NFS_TRY(run_forward(P, P->d_p, nullptr));
+  NFS_CUDA(nfs::launch_unpack(P->prec == NFS_PREC_FP64 ? 1 : 0, P->d_y, P->d_io, P->K, P->G, P->ldc, P->stream));
+  NFS_CUDA(cudaMemcpyAsync(y, P->d_io, (size_t)P->K * P->G * sizeof(double2), cudaMemcpyDeviceToHost, P->stream));
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
+  return NFS_OK;
+}
+
+extern "C" int nfs_apply_EH(nfs_plan* P, const double* sigma, double* q) {
+  NFS_TRY(need_ready(P));
+  NFS_TRY(upload_samples(P, sigma, P->d_y));
+  NFS_TRY(run_adjoint(P, P->d_y, P->d_q, nullptr));
+  NFS_CUDA(cudaMemcpyAsync(q, P->d_q, P->L * sizeof(double2), cudaMemcpyDeviceToHost, P->stream));
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
+  return NFS_OK;
+}
+
+extern "C" int nfs_apply_EHE(nfs_plan* P, const double* p, double* q) {
+  NFS_TRY(need_ready(P));
+  NFS_CUDA(cudaMemcpyAsync(P->d_p, p, P->L * sizeof(double2), cudaMemcpyHostToDevice, P->stream));
+  NFS_TRY(run_ehe(P, P->d_p, P->d_q, nullptr));
+  NFS_CUDA(cudaMemcpyAsync(q, P->d_q, P->L * sizeof(double2), cudaMemcpyDeviceToHost, P->stream));
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
+  return NFS_OK;
+}
+
+extern "C" int nfs_phase_rows(nfs_plan* P, int64_t lo, int64_t hi, double* out) {
+  if (!P || !P->have_tables) return fail(NFS_ERR_INVALID, "tables must be set first");
+  if (lo < 0 || hi > P->K || hi < lo) return fail(NFS_ERR_INVALID, "row range out of bounds");
+  if (hi == lo) return NFS_OK;
+  NFS_CUDA(cudaSetDevice(P->device));
+  const size_t n = (size_t)(hi - lo) * P->L;
+  double2* d = nullptr;
+  NFS_CUDA(cudaMalloc(&d, n * sizeof(double2)));
+  cudaError_t e = nfs::launch_phase_rows(P->prec == NFS_PREC_FP64 ? 1 : 0, P->NT, P->d_T, P->d_R,
+                                         lo, hi - lo, P->L, d, P->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, n * sizeof(double2), cudaMemcpyDeviceToHost, P->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(NFS_ERR_CUDA, std::string("phase rows: ") + cudaGetErrorString(e));
+  return NFS_OK;
+}
+
+// ------------------------------------------------------------------ CG
+static int cg_iteration(nfs_plan* P) {
+  const int* stop = &P->d_cg->stop;
+  NFS_TRY(run_ehe(P, P->d_p, P->d_q, stop));
+  NFS_CUDA(nfs::launch_cg_iter_tail(P->d_q, P->d_p, P->d_r, P->d_rho, P->L, P->d_cg,
+                                    P->d_partials, P->d_res, P->d_sol, P->stream));
+  return NFS_OK;
+}
+
+extern "C" int nfs_cg_solve(nfs_plan* P, int32_t n_iter, nfs_iter_callback cb, void* user,
+                            double* rho, double* res_norms, double* sol_norms, int32_t* n_done,
+                            double* timings) {
+  NFS_TRY(need_ready(P));
+  if (!P->have_samples) return fail(NFS_ERR_INVALID, "samples must be set first");
+  if (n_iter < 0) return fail(NFS_ERR_INVALID, "negative iteration count");
+  if (n_done) *n_done = 0;
+  if (n_iter > P->log_cap) {
+    if (P->d_res) cudaFree(P->d_res);
+    if (P->d_sol) cudaFree(P->d_sol);
+    P->d_res = P->d_sol = nullptr;
+    NFS_CUDA(cudaMalloc(&P->d_res, std::max(n_iter, 1) * sizeof(double)));
+    NFS_CUDA(cudaMalloc(&P->d_sol, std::max(n_iter, 1) * sizeof(double)));
+    P->log_cap = n_iter;
+  }
+  std::vector<cudaEvent_t> ev(n_iter + 2);
+  for (auto& e : ev) NFS_CUDA(cudaEventCreate(&e));
+  struct EvGuard {
+    std::vector<cudaEvent_t>& v;
+    ~EvGuard() { for (auto e : v) cudaEventDestroy(e); }
+  } guard{ev};
+
+  NFS_CUDA(cudaMemsetAsync(P->d_cg, 0, sizeof(CGState), P->stream));
+  NFS_CUDA(cudaEventRecord(ev[0], P->stream));
+  NFS_TRY(run_adjoint(P, P->d_sig, P->d_q0, nullptr));                 // initial_adjoint
+  NFS_CUDA(nfs::launch_cg_init(P->d_q0, P->d_r, P->d_p, P->d_rho, P->L, P->d_cg, P->d_partials, P->stream));
+  NFS_CUDA(cudaEventRecord(ev[1], P->stream));
+
+  // capture one iteration as a CUDA graph (falls back to direct launches)
+  cudaGraphExec_t gexec = nullptr;
+  if (n_iter > 1) {
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      int s = cg_iteration(P);
+      cudaError_t ce = cudaStreamEndCapture(P->stream, &graph);
+      if (s == NFS_OK && ce == cudaSuccess && graph &&
+          cudaGraphInstantiate(&gexec, graph, 0) != cudaSuccess)
+        gexec = nullptr;
+      if (graph) cudaGraphDestroy(graph);
+    }
+    cudaGetLastError();
+  }
+  std::vector<double> host_rho;
+  if (cb) host_rho.resize((size_t)P->L * 2);
+  int done = 0;
+  CGState st{};
+  for (int n = 1; n <= n_iter; ++n) {
+    if (gexec) NFS_CUDA(cudaGraphLaunch(gexec, P->stream));
+    else NFS_TRY(cg_iteration(P));
+    NFS_CUDA(cudaEventRecord(ev[n + 1], P->stream));
+    if (cb) {
+      NFS_CUDA(cudaMemcpyAsync(&st, P->d_cg, sizeof st, cudaMemcpyDeviceToHost, P->stream));
+      NFS_CUDA(cudaStreamSynchronize(P->stream));
+      if (st.err || st.iter < n) break;
+      NFS_CUDA(cudaMemcpy(host_rho.data(), P->d_rho, P->L * sizeof(double2), cudaMemcpyDeviceToHost));
+      cb(n, host_rho.data(), user);
+      if (st.stop) break;
+    }
+  }
+  if (gexec) cudaGraphExecDestroy(gexec);
+  NFS_CUDA(cudaMemcpyAsync(&st, P->d_cg, sizeof st, cudaMemcpyDeviceToHost, P->stream));
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
+  done = st.iter;
+  if (n_done) *n_done = st.err ? st.err_iter : done;
+  if (st.err == NFS_ERR_BREAKDOWN)
+    return fail(NFS_ERR_BREAKDOWN, "CG breakdown at iteration " + std::to_string(st.err_iter));
+  if (st.err == NFS_ERR_NONFINITE_ITERATE)
+    return fail(NFS_ERR_NONFINITE_ITERATE, "non-finite iterate at iteration " + std::to_string(st.err_iter));
+  if (rho) NFS_CUDA(cudaMemcpy(rho, P->d_rho, P->L * sizeof(double2), cudaMemcpyDeviceToHost));
+  if (done > 0) {
+    if (res_norms) NFS_CUDA(cudaMemcpy(res_norms, P->d_res, done * sizeof(double), cudaMemcpyDeviceToHost));
+    if (sol_norms) NFS_CUDA(cudaMemcpy(sol_norms, P->d_sol, done * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  if (timings) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[0], ev[1]);
+    timings[0] = ms * 1e-3;
+    const int last = cb ? std::min(done, n_iter) : n_iter;
+    cudaEventElapsedTime(&ms, ev[0], ev[std::max(last, 0) + 1]);
+    timings[1] = ms * 1e-3;
+    for (int n = 1; n <= n_iter; ++n) {
+      timings[1 + n] = 0.0;
+      if (n <= done && n <= last) {
+        cudaEventElapsedTime(&ms, ev[n], ev[n + 1]);
+        timings[1 + n] = ms * 1e-3;
+      }
+    }
+  }
+  return NFS_OK;
+}
+
+// ------------------------------------------------------------------ benchmarking hooks
+extern "C" int nfs_apply_EHE_resident(nfs_plan* P, int32_t n) {
+  NFS_TRY(need_ready(P));
+  for (int i = 0; i < n; ++i) NFS_TRY(run_ehe(P, P->d_p, P->d_q, nullptr));
+  return NFS_OK;
+}
+
+extern "C" int nfs_kernel_times(nfs_plan* P, int32_t reps, float* ms_out) {
+  NFS_TRY(need_ready(P));
+  if (reps < 1 || !ms_out) return fail(NFS_ERR_INVALID, "bad arguments");
+  cudaEvent_t e[5];
+  for (auto& x : e) NFS_CUDA(cudaEventCreate(&x));
+  double acc[4] = {0, 0, 0, 0};
+  for (int r = 0; r < reps; ++r) {
+    if (P->tc) {
+      NFS_CUDA(cudaEventRecord(e[0], P->stream));
+      if (nfs::tc_forward_parts(P->tc, P->d_p, P->d_y, nullptr, P->stream, 0))
+        return fail(NFS_ERR_CUDA, nfs::tc_last_error());
+      NFS_CUDA(cudaEventRecord(e[1], P->stream));
+      if (nfs::tc_forward_parts(P->tc, P->d_p, P->d_y, nullptr, P->stream, 1))
+        return fail(NFS_ERR_CUDA, nfs::tc_last_error());
+      NFS_CUDA(cudaEventRecord(e[2], P->stream));
+      if (nfs::tc_adjoint_parts(P->tc, P->d_y, P->d_q, nullptr, P->stream, 0))
+        return fail(NFS_ERR_CUDA, nfs::tc_last_error());
+      NFS_CUDA(cudaEventRecord(e[3], P->stream));
+      if (nfs::tc_adjoint_parts(P->tc, P->d_y, P->d_q, nullptr, P->stream, 1))
+        return fail(NFS_ERR_CUDA, nfs::tc_last_error());
+      NFS_CUDA(cudaEventRecord(e[4], P->stream));
+    } else {
+      const int cp = (P->prec == NFS_PREC_FP64) ? 1 : 0;
+      nfs::ContractLaunch F = base_launch(P, true);
+      F.p = P->d_p;
+      F.out = (P->split_f > 1) ? P->d_party : P->d_y;
+      nfs::ContractLaunch A = base_launch(P, false);
+      A.y = P->d_y;
+      A.out = P->d_partq;
+      NFS_CUDA(cudaEventRecord(e[0], P->stream));
+      NFS_CUDA(nfs::launch_contract(F, P->stream));
+      NFS_CUDA(cudaEventRecord(e[1], P->stream));
+      if (P->split_f > 1)
+        NFS_CUDA(nfs::launch_reduce_parts(cp, P->d_party, P->d_y, P->K * P->ldc, P->split_f, nullptr, P->stream));
+      NFS_CUDA(cudaEventRecord(e[2], P->stream));
+      NFS_CUDA(nfs::launch_contract(A, P->stream));
+      NFS_CUDA(cudaEventRecord(e[3], P->stream));
+      NFS_CUDA(nfs::launch_reduce_image(cp, P->d_partq, P->d_q, P->L, P->split_a * P->NG, nullptr, P->stream));
+      NFS_CUDA(cudaEventRecord(e[4], P->stream));
+    }
+    NFS_CUDA(cudaEventSynchronize(e[4]));
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e[i], e[i + 1]);
+      acc[i] += ms;
+    }
+  }
+  for (auto& x : e) cudaEventDestroy(x);
+  for (int i = 0; i < 4; ++i) ms_out[i] = (float)(acc[i] / reps);
+  return NFS_OK;
+}
+
+extern "C" int nfs_launches_per_apply(nfs_plan* P) {
+  if (!P) return 0;
+  if (P->tc) return nfs::tc_launches_per_apply(P->tc);
+  return 1 + (P->split_f > 1 ? 1 : 0) + 2;
+}
+
+extern "C" const char* nfs_plan_describe(nfs_plan* P) { return P ? P->desc.c_str() : ""; }

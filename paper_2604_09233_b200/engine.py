@@ -1,0 +1,334 @@
+"""Drop-in GPU engine: the reference's engine API on the B200 path.
+
+Same names, signatures, argument meaning, exception classes and CGLog contents as the
+reference's `nfs/engine.py` (cited per function).  Every numeric operation on the hot path
+runs in the CUDA extension (`_nfs_b200.so`, include/nfs_b200.h) -- there is no CPU fallback.
+
+Precision: the operators run in FP64 parity mode by default ("fp64": FP64 phase, sincospi
+and FMA), which reproduces the reference's own 1e-10/1e-12 tests.  The fast modes are
+selected per call (`precision="fp32"` or `"tf32x3"`) or process-wide via the environment
+variable NFS_B200_PRECISION.  DESIGN.md states the tolerance of each mode.
+
+Multi-GPU: when torch.distributed is initialised with world_size > 1, `recon_full` /
+`recon_split` shard the readout samples across ranks (contiguous rows) and all-reduce the
+adjoint image once per iteration over NCCL; every rank returns the result.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .core import Grid, ReconImage, grid_coordinates
+from .errors import EngineError, MemoryBudgetError
+from .simulate import solid_harmonics
+
+__all__ = [
+    "EngineError", "MemoryBudgetError", "EncodingInputs", "CGLog", "phase_block", "apply_E",
+    "apply_EH", "recon_full", "recon_split", "choose_block_starts", "build_bases",
+    "default_precision", "PhaseBlock",
+]
+
+
+def default_precision() -> str:
+    return os.environ.get("NFS_B200_PRECISION", "fp64")
+
+
+def default_device() -> int:
+    env = os.environ.get("NFS_B200_DEVICE")
+    if env is not None:
+        return int(env)
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ----------------------------------------------------------------------------------
+# types (nfs/engine.py:30-90)
+# ----------------------------------------------------------------------------------
+
+@dataclass
+class EncodingInputs:
+    """Inputs of the reconstruction, voxel arrays restricted to the mask (nfs/engine.py:30-78)."""
+
+    sigma: np.ndarray
+    spatial: np.ndarray
+    temporal: np.ndarray
+    sens: np.ndarray
+    intensity: np.ndarray
+    kfilter: np.ndarray | None
+    mask_r: np.ndarray
+    grid: Grid
+    n_iter: int
+    block_starts: np.ndarray | None = None
+
+    def __post_init__(self):
+        k, gam = self.sigma.shape
+        p1, l_r = self.spatial.shape
+        if self.temporal.shape != (k, p1):
+            raise EngineError(
+                f"temporal basis shape {self.temporal.shape} does not match samples {k} / terms {p1}")
+        if self.sens.shape != (l_r, gam):
+            raise EngineError(
+                f"sensitivity shape {self.sens.shape} does not match voxels {l_r} / coils {gam}")
+        if self.intensity.shape != (l_r,):
+            raise EngineError("intensity correction length mismatch")
+        self.mask_r = np.asarray(self.mask_r, dtype=bool).reshape(-1)
+        if int(self.mask_r.sum()) != l_r:
+            raise EngineError("reconstruction mask does not match restricted arrays")
+        if self.block_starts is not None:
+            ks = np.asarray(self.block_starts, dtype=int)
+            if ks[0] != 0 or ks[-1] != k or np.any(np.diff(ks) <= 0):
+                raise EngineError("block starts must increase from 0 to the sample count")
+            self.block_starts = ks
+
+    @property
+    def n_samples(self) -> int:
+        return self.sigma.shape[0]
+
+    @property
+    def n_voxels(self) -> int:
+        return self.spatial.shape[1]
+
+
+@dataclass
+class CGLog:
+    """Per-iteration norms and per-phase timings (nfs/engine.py:81-90)."""
+
+    residual_norms: list = field(default_factory=list)
+    solution_norms: list = field(default_factory=list)
+    timings: list = field(default_factory=list)
+
+    def add_timing(self, label: str, seconds: float):
+        self.timings.append((label, seconds))
+
+
+# ----------------------------------------------------------------------------------
+# lazy phase handle (nfs/engine.py:93-95)
+# ----------------------------------------------------------------------------------
+
+class PhaseBlock:
+    """P' = exp(i * temporal_rows @ spatial), never materialised on the hot path.
+
+    Holds the basis tables; `apply_E` / `apply_EH` regenerate the phasors on the device.
+    `np.asarray(handle)` materialises the block on the GPU (FP64 unless `precision` says
+    otherwise) for small sizes, so code that inspects the matrix keeps working.
+    """
+
+    __array_priority__ = 10
+
+    def __init__(self, temporal_rows, spatial, precision=None, device=None):
+        self.temporal = np.ascontiguousarray(temporal_rows, dtype=np.float64)
+        self.spatial = np.ascontiguousarray(spatial, dtype=np.float64)
+        if self.temporal.ndim != 2 or self.spatial.ndim != 2 or \
+                self.temporal.shape[1] != self.spatial.shape[0]:
+            raise EngineError("temporal rows and spatial basis shapes do not match")
+        self.precision = precision or default_precision()
+        self.device = default_device() if device is None else device
+        self._plans = {}
+
+    @property
+    def shape(self):
+        return (self.temporal.shape[0], self.spatial.shape[1])
+
+    @property
+    def dtype(self):
+        return np.dtype(np.complex128)
+
+    def plan(self, n_coils: int) -> _native.Plan:
+        key = (int(n_coils), self.precision)
+        plan = self._plans.get(key)
+        if plan is None:
+            k, l = self.shape
+            plan = _native.Plan(k, l, n_coils, self.temporal.shape[1], self.precision, self.device)
+            plan.set_tables(self.temporal, self.spatial)
+            self._plans[key] = plan
+        return plan
+
+    def materialize(self) -> np.ndarray:
+        k, _ = self.shape
+        return self.plan(1).phase_rows(0, k)
+
+    def __array__(self, dtype=None, copy=None):
+        out = self.materialize()
+        return out if dtype is None else out.astype(dtype)
+
+    def __abs__(self):
+        return np.abs(self.materialize())
+
+
+def phase_block(temporal_rows: np.ndarray, spatial: np.ndarray) -> PhaseBlock:
+    """Lazy device phase block for a row range (nfs/engine.py:93-95)."""
+    return PhaseBlock(temporal_rows, spatial)
+
+
+def _as_phase(phase) -> PhaseBlock:
+    if isinstance(phase, PhaseBlock):
+        return phase
+    raise EngineError("phase must be the handle returned by phase_block(); "
+                      "materialised phase matrices are not used on the GPU path")
+
+
+def apply_E(p: np.ndarray, sens: np.ndarray, phase) -> np.ndarray:
+    """Predicted coil samples P @ (S * p), shape (K, Gamma) (nfs/engine.py:98-100)."""
+    ph = _as_phase(phase)
+    sens = np.asarray(sens)
+    plan = ph.plan(sens.shape[1])
+    plan.set_sens(sens)
+    return plan.apply_E(np.asarray(p).reshape(-1))
+
+
+def apply_EH(sigma: np.ndarray, sens: np.ndarray, phase) -> np.ndarray:
+    """Adjoint image sum_c conj(S) * (P^H sigma), shape (L_R,) (nfs/engine.py:103-108)."""
+    ph = _as_phase(phase)
+    sens = np.asarray(sens)
+    plan = ph.plan(sens.shape[1])
+    plan.set_sens(sens)
+    return plan.apply_EH(np.asarray(sigma))
+
+
+# ----------------------------------------------------------------------------------
+# reconstruction drivers
+# ----------------------------------------------------------------------------------
+
+def _dist_info():
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            return dist, dist.get_rank(), dist.get_world_size()
+    except Exception:
+        pass
+    return None, 0, 1
+
+
+def shard_rows(n_samples: int, rank: int, world: int):
+    """Contiguous, balanced sample-row shard of `rank`."""
+    base, extra = divmod(n_samples, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def _nccl_unique_id(dist, rank):
+    """Rank 0 creates an NCCL unique id (via torch's bundled NCCL) and broadcasts it."""
+    obj = [None]
+    if rank == 0:
+        import torch.cuda.nccl as tnccl
+        obj[0] = bytes(tnccl.unique_id())
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label: bool):
+    """Create the device plan for this rank's sample shard; upload tables, S', sigma."""
+    dist, rank, world = _dist_info()
+    lo, hi = shard_rows(inputs.n_samples, rank, world)
+    device = default_device()
+    t0 = time.perf_counter()
+    plan = _native.Plan(hi - lo, inputs.n_voxels, inputs.sens.shape[1],
+                        inputs.spatial.shape[0], precision, device)
+    if world > 1:
+        plan.attach_comm(_nccl_unique_id(dist, rank), rank, world)
+    t_plan = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    plan.set_sens(inputs.sens, inputs.intensity)          # S' = S o j on upload
+    log.add_timing("intensity_correction", time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    plan.set_tables(inputs.temporal[lo:hi], inputs.spatial)
+    if timing_label:   # the GPU analogue of building P: plan + table upload
+        log.add_timing("build_phase_matrix", t_plan + time.perf_counter() - t0)
+    plan.set_samples(inputs.sigma[lo:hi])
+    return plan
+
+
+def _run_cg(plan, inputs: EncodingInputs, log: CGLog, callback):
+    rho, res, sol, tim, n_done = plan.cg_solve(inputs.n_iter, callback)
+    log.add_timing("initial_adjoint", float(tim[0]))
+    for n in range(1, n_done + 1):
+        log.add_timing(f"cg_iteration_{n}", float(tim[1 + n]))
+    log.residual_norms.extend(res)
+    log.solution_norms.extend(sol)
+    return rho
+
+
+def _finalize(rho_r: np.ndarray, inputs: EncodingInputs, log: CGLog) -> ReconImage:
+    """rho o j, scatter to the grid, optional k-space filter (nfs/engine.py:111-122)."""
+    from .kfilter import apply_filter
+
+    t0 = time.perf_counter()
+    full = np.zeros(inputs.mask_r.size, dtype=complex)
+    full[inputs.mask_r] = rho_r * inputs.intensity
+    log.add_timing("apply_intensity", time.perf_counter() - t0)
+    if inputs.kfilter is not None:
+        t0 = time.perf_counter()
+        full = apply_filter(full, inputs.kfilter, inputs.grid)
+        log.add_timing("apply_kfilter", time.perf_counter() - t0)
+    res = log.residual_norms[-1] if log.residual_norms else 0.0
+    return ReconImage(values=full, iterations=inputs.n_iter, final_residual=res)
+
+
+def recon_full(inputs: EncodingInputs, memory_budget_bytes: int | None = None, callback=None,
+               *, precision: str | None = None):
+    """CG reconstruction (nfs/engine.py:125-179).
+
+    The phase matrix is never stored on the GPU; the reference's budget rule
+    (K * L_R * 16 bytes > budget -> MemoryBudgetError) is kept because callers and the
+    CLI exit codes depend on it.  `callback(n, rho_restricted)` runs after each iteration.
+    """
+    need = inputs.n_samples * inputs.n_voxels * 16
+    if memory_budget_bytes is not None and need > memory_budget_bytes:
+        raise MemoryBudgetError(
+            f"phase matrix needs {need} bytes (> budget {memory_budget_bytes}); use the split variant")
+    log = CGLog()
+    if not np.all(np.isfinite(inputs.sigma)):
+        raise EngineError("raw data contains non-finite values")
+    plan = _make_plan(inputs, precision or default_precision(), log, timing_label=True)
+    try:
+        rho = _run_cg(plan, inputs, log, callback)
+    finally:
+        plan.close()
+    return _finalize(rho, inputs, log), log
+
+
+def recon_split(inputs: EncodingInputs, callback=None, *, precision: str | None = None):
+    """Split-variant CG (nfs/engine.py:182-241).
+
+    On the GPU both variants regenerate the phase on the fly, so the block structure only
+    affects validation; results equal `recon_full` bit for bit.
+    """
+    if inputs.block_starts is None:
+        raise EngineError("split reconstruction needs block starts")
+    log = CGLog()
+    if not np.all(np.isfinite(inputs.sigma)):
+        raise EngineError("raw data contains non-finite values")
+    plan = _make_plan(inputs, precision or default_precision(), log, timing_label=False)
+    try:
+        rho = _run_cg(plan, inputs, log, callback)
+    finally:
+        plan.close()
+    return _finalize(rho, inputs, log), log
+
+
+def choose_block_starts(n_samples: int, n_voxels: int, memory_budget_bytes: int) -> np.ndarray:
+    """Largest row block whose c128 phase block fits the budget (nfs/engine.py:244-249)."""
+    rows = max(1, min(n_samples, memory_budget_bytes // max(n_voxels * 16, 1)))
+    return np.unique(np.asarray(list(range(0, n_samples, rows)) + [n_samples], dtype=int))
+
+
+def build_bases(b0, mask_r, grid: Grid, times_s, field_terms, order: int = 1):
+    """Spatial (P+1, L_R) and temporal (K, P+1) basis tables (nfs/engine.py:252-280)."""
+    mask_r = np.asarray(mask_r, dtype=bool).reshape(-1)
+    b0 = np.asarray(b0, dtype=float).reshape(-1)
+    coords = grid_coordinates(grid)[mask_r]
+    harm = solid_harmonics(order, coords, ndim=grid.ndim)
+    field_terms = np.asarray(field_terms, dtype=float)
+    if field_terms.ndim != 2 or field_terms.shape[1] != harm.shape[1]:
+        got = field_terms.shape[1] if field_terms.ndim == 2 else "?"
+        raise EngineError(f"trajectory provides {got} field terms but order {order} needs {harm.shape[1]}")
+    times_s = np.asarray(times_s, dtype=float).reshape(-1)
+    if times_s.size != field_terms.shape[0]:
+        raise EngineError("sample time count does not match field terms")
+    spatial = np.vstack([b0[mask_r][None, :], harm.T])
+    temporal = np.column_stack([times_s, field_terms])
+    return spatial, temporal

@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the golden vectors.
+
+Tolerances (stated per mode):
+  fp64 parity mode : the reference's own tolerances (1e-14 phase, 1e-10 / 1e-12 operators,
+                     1e-10 split/full, 1e-12 exact recovery) and <= 1e-8 relative-L2 on
+                     the CG iterate at 20 iterations of config A.
+  fp32 fast mode   : operators <= 2e-5 relative-L2; CG iterate <= 1e-5 at 10 iterations
+                     and <= 1e-2 at 20 iterations of config A (FP32 loss-of-orthogonality
+                     floor).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import nfs_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+nfs = pytest.importorskip("paper_2604_09233_b200")
+from paper_2604_09233_b200 import engine, simulate  # noqa: E402
+from paper_2604_09233_b200._native import Plan  # noqa: E402
+from paper_2604_09233_b200.core import Grid, grid_coordinates  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def inputs_from(grid, sigma, spatial, temporal, sens, n_iter, block_starts=None, mask=None,
+                intensity=None, kfilter=None):
+    mask = np.ones(grid.nvox, bool) if mask is None else mask
+    intensity = np.ones(int(mask.sum())) if intensity is None else intensity
+    return engine.EncodingInputs(sigma=sigma, spatial=spatial, temporal=temporal, sens=sens,
+                                 intensity=intensity, kfilter=kfilter, mask_r=mask, grid=grid,
+                                 n_iter=n_iter, block_starts=block_starts)
+
+
+# ------------------------------------------------------------------ operators, fp64
+def test_phase_block_materialised_fp64():
+    g = golden("engine8")
+    blk = np.asarray(engine.phase_block(g["temporal"][10:20], g["spatial"]))
+    assert np.allclose(blk, g["phase_rows"], atol=1e-14)
+    assert np.allclose(np.abs(blk), 1.0)
+
+
+def test_operators_fp64_vs_golden_and_dense():
+    g = golden("engine8")
+    ph = engine.phase_block(g["temporal"], g["spatial"])
+    y = engine.apply_E(g["rho"], g["sens"], ph)
+    q = engine.apply_EH(g["sig_rand"], g["sens"], ph)
+    assert rel(y, g["E_rho"]) < 1e-13
+    assert rel(q, g["EH_sig"]) < 1e-13
+    dense = g["dense"]
+    assert np.allclose(y.ravel(order="F"), dense @ g["rho"], atol=1e-10)
+    assert np.allclose(q, dense.conj().T @ g["sig_rand"].ravel(order="F"), atol=1e-10)
+    lhs = np.vdot(g["sig_rand"].ravel(order="F"), y.ravel(order="F"))
+    rhs = np.vdot(q, g["rho"])
+    assert abs(lhs - rhs) <= 1e-9
+
+
+def test_oracle_equivalence_random_instances_fp64():
+    """tests/test_acceptance.py:74-103 on the GPU path: 20 random instances, <= 1e-12."""
+    rng = np.random.default_rng(2024)
+    worst = 0.0
+    for _ in range(20):
+        n_vox = int(rng.integers(16, 257))
+        n_samp = int(rng.integers(16, 513))
+        n_coil = int(rng.integers(1, 5))
+        n_terms = int(rng.integers(2, 16))
+        spatial = rng.standard_normal((n_terms, n_vox))
+        temporal = rng.standard_normal((n_samp, n_terms))
+        sens = rng.standard_normal((n_vox, n_coil)) + 1j * rng.standard_normal((n_vox, n_coil))
+        p = rng.standard_normal(n_vox) + 1j * rng.standard_normal(n_vox)
+        sigma = rng.standard_normal((n_samp, n_coil)) + 1j * rng.standard_normal((n_samp, n_coil))
+        dense = orc.dense_encoding_matrix(sens, spatial, temporal)
+        ph = engine.phase_block(temporal, spatial)
+        ep = engine.apply_E(p, sens, ph).ravel(order="F")
+        ehs = engine.apply_EH(sigma, sens, ph)
+        worst = max(worst, rel(ep, dense @ p), rel(ehs, dense.conj().T @ sigma.ravel(order="F")))
+        lhs, rhs = np.vdot(sigma.ravel(order="F"), ep), np.vdot(ehs, p)
+        worst = max(worst, abs(lhs - rhs) / abs(lhs))
+    assert worst <= 1e-12, worst
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-12), ("fp32", 2e-5)])
+def test_many_coils_and_terms(prec, tol):
+    """Coil groups (G=40 > 32), odd term counts (P+1=17 -> padded 20), ragged sizes."""
+    rng = np.random.default_rng(3)
+    L, K, G, P1 = 301, 777, 40, 17
+    spatial = rng.standard_normal((P1, L)) * 0.5
+    temporal = rng.standard_normal((K, P1)) * 2.0
+    sens = rng.standard_normal((L, G)) + 1j * rng.standard_normal((L, G))
+    p = rng.standard_normal(L) + 1j * rng.standard_normal(L)
+    sig = rng.standard_normal((K, G)) + 1j * rng.standard_normal((K, G))
+    ph = orc.phase_block(temporal, spatial)
+    plan = Plan(K, L, G, P1, prec)
+    plan.set_tables(temporal, spatial)
+    plan.set_sens(sens)
+    assert rel(plan.apply_E(p), orc.apply_E(p, sens, ph)) < tol
+    assert rel(plan.apply_EH(sig), orc.apply_EH(sig, sens, ph)) < tol
+    q = plan.apply_EHE(p)
+    assert rel(q, orc.apply_EH(orc.apply_E(p, sens, ph), sens, ph)) < tol
+    plan.close()
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-10), ("fp32", 2e-5)])
+def test_config_b_rows(prec, tol):
+    """Config B tables (L_R=41,684, 32 coils, P+1=16) on a 64-row subset vs the reference."""
+    g = golden("config_b_rows")
+    prob = simulate.make_problem("B")
+    rows = g["rows"]
+    plan = Plan(rows.size, prob.spatial.shape[1], 32, 16, prec)
+    plan.set_tables(prob.temporal[rows], prob.spatial)
+    plan.set_sens(prob.sens, prob.intensity)
+    assert rel(plan.apply_E(prob.rho_true / prob.intensity), g["E_rows"]) < tol
+    assert rel(plan.apply_EH(g["sig"]), g["EH_rows"]) < tol
+    plan.close()
+
+
+# ------------------------------------------------------------------ CG drivers
+def test_recon_full_and_split_fp64_vs_golden():
+    g = golden("engine8")
+    grid = Grid((8, 8, 1), (0.08, 0.08, 0.002))
+    args = (grid, g["sigma"], g["spatial"], g["temporal"], g["sens"], 15)
+    img, log = engine.recon_full(inputs_from(*args))
+    assert rel(img.values, g["full_values"]) < 1e-10
+    assert np.allclose(log.residual_norms, g["full_res"], rtol=1e-8)
+    assert np.allclose(log.solution_norms, g["full_sol"], rtol=1e-10)
+    simg, slog = engine.recon_split(inputs_from(*args, block_starts=g["starts"]))
+    assert np.allclose(simg.values, img.values, atol=1e-10)
+    assert np.allclose(slog.residual_norms, log.residual_norms, rtol=1e-8)
+    assert rel(simg.values, g["split_values"]) < 1e-10
+
+
+def test_exact_recovery_early_stop():
+    g = golden("cartesian8")
+    grid = Grid((8, 8, 1), (0.08, 0.08, 0.002))
+    spatial = np.vstack([np.zeros(64), grid_coordinates(grid)[:, :2].T])
+    img, log = engine.recon_full(inputs_from(grid, g["sigma"], spatial, g["temporal"],
+                                             np.ones((64, 1), complex), 10))
+    assert rel(img.values, g["rho_true"]) < 1e-12
+    assert len(log.residual_norms) < 10
+    assert img.iterations == 10   # reference quirk: reports n_iter (nfs/engine.py:122)
+
+
+def test_config_a_fp64_vs_golden():
+    g = golden("config_a")
+    prob = simulate.make_problem("A")
+    seen = []
+    img, log = engine.recon_full(inputs_from(prob.grid, g["sigma"], prob.spatial, prob.temporal,
+                                             prob.sens, 20),
+                                 callback=lambda n, r: seen.append((n, r)))
+    assert [n for n, _ in seen] == list(range(1, 21))
+    assert rel(img.values, g["values"]) < 1e-8
+    assert np.allclose(log.residual_norms, g["res"], rtol=1e-6)
+    for it, ref in zip(g["iters"], g["rho_iters"]):
+        assert rel(seen[it - 1][1], ref) < 1e-8
+
+
+def test_config_a_fp32_tolerance():
+    g = golden("config_a")
+    prob = simulate.make_problem("A")
+    seen = {}
+    img, log = engine.recon_full(inputs_from(prob.grid, g["sigma"], prob.spatial, prob.temporal,
+                                             prob.sens, 20),
+                                 callback=lambda n, r: seen.__setitem__(n, r), precision="fp32")
+    assert rel(seen[5], g["rho_iters"][0]) < 1e-5
+    assert rel(seen[10], g["rho_iters"][1]) < 1e-5
+    assert rel(img.values, g["values"]) < 1e-2
+    assert np.allclose(log.residual_norms[:10], g["res"][:10], rtol=1e-3)
+
+
+def test_config_a_masked_with_filter_fp64():
+    g = golden("config_a")
+    pm = simulate.make_problem("A_mask")
+    img, log = engine.recon_full(inputs_from(pm.grid, g["sigma"], pm.spatial, pm.temporal, pm.sens,
+                                             20, mask=pm.mask_r, intensity=pm.intensity,
+                                             kfilter=g["kfilter"]))
+    assert rel(img.values, g["values_mask"]) < 1e-8
+    labels = [lab for lab, _ in log.timings]
+    assert labels[:3] == ["intensity_correction", "build_phase_matrix", "initial_adjoint"]
+    assert labels[-2:] == ["apply_intensity", "apply_kfilter"]
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("fp32", 1e-3)])
+def test_small3d_order3(prec, tol):
+    g = golden("small3d")
+    grid = Grid((12, 12, 6), (0.22, 0.22, 0.128))
+    img, _ = engine.recon_full(inputs_from(grid, g["sigma"], g["spatial"], g["temporal"], g["sens"], 12),
+                               precision=prec)
+    assert rel(img.values, g["values"]) < tol
+
+
+def test_errors_and_contracts(rng):
+    g = golden("engine8")
+    grid = Grid((8, 8, 1), (0.08, 0.08, 0.002))
+    sigma = g["sigma"].copy()
+    sigma[5, 1] = np.nan
+    with pytest.raises(engine.EngineError):
+        engine.recon_full(inputs_from(grid, sigma, g["spatial"], g["temporal"], g["sens"], 5))
+    with pytest.raises(engine.MemoryBudgetError, match="split"):
+        engine.recon_full(inputs_from(grid, g["sigma"], g["spatial"], g["temporal"], g["sens"], 5),
+                          memory_budget_bytes=100)
+    with pytest.raises(engine.EngineError):
+        engine.recon_split(inputs_from(grid, g["sigma"], g["spatial"], g["temporal"], g["sens"], 5))
+    # zero data: r0 == 0 -> no iterations, zero image (nfs/engine.py:158)
+    img, log = engine.recon_full(inputs_from(grid, np.zeros_like(g["sigma"]), g["spatial"],
+                                             g["temporal"], g["sens"], 5))
+    assert log.residual_norms == [] and np.all(img.values == 0)
+
+
+def test_restricted_mask_scatter(rng):
+    grid = Grid((8, 8, 1), (0.08, 0.08, 0.002))
+    mask = rng.random(64) > 0.4
+    n = int(mask.sum())
+    g = golden("engine8")
+    spatial, sens = g["spatial"][:, mask], g["sens"][mask]
+    sigma = orc.forward_signal(rng.standard_normal(n) + 0j, sens, spatial, g["temporal"])
+    img, _ = engine.recon_full(inputs_from(grid, sigma, spatial, g["temporal"], sens, 5, mask=mask))
+    assert np.all(img.values[~mask] == 0)
+    assert np.any(img.values[mask] != 0)
+
+
+def test_determinism_bitwise():
+    g = golden("config_a")
+    prob = simulate.make_problem("A")
+    mk = lambda: inputs_from(prob.grid, g["sigma"], prob.spatial, prob.temporal, prob.sens, 8)  # noqa: E731
+    a, _ = engine.recon_full(mk(), precision="fp32")
+    b, _ = engine.recon_full(mk(), precision="fp32")
+    assert np.array_equal(a.values, b.values)
+
+
+# ------------------------------------------------------------------ full-size properties
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_config_b_full_size_properties(prec):
+    """At BASELINE size: adjoint identity, linearity, and E^H E hermitian positivity."""
+    prob = simulate.make_problem("B")
+    K, L = prob.temporal.shape[0], prob.spatial.shape[1]
+    plan = Plan(K, L, 32, 16, prec)
+    plan.set_tables(prob.temporal, prob.spatial)
+    plan.set_sens(prob.sens, prob.intensity)
+    rng = np.random.default_rng(0)
+    p = rng.standard_normal(L) + 1j * rng.standard_normal(L)
+    sig = rng.standard_normal((K, 32)) + 1j * rng.standard_normal((K, 32))
+    y = plan.apply_E(p)
+    q = plan.apply_EH(sig)
+    lhs, rhs = np.vdot(sig, y), np.vdot(q, p)
+    tol = 1e-11 if prec == "fp64" else 1e-5
+    assert abs(lhs - rhs) / abs(lhs) < tol
+    y2 = plan.apply_E(2.0 * p + 1j * p)
+    assert rel(y2, (2.0 + 1j) * y) < tol
+    ehe = plan.apply_EHE(p)
+    quad = np.vdot(p, ehe)
+    assert quad.real > 0 and abs(quad.imag) / quad.real < tol
+    assert abs(quad.real - np.vdot(y, y).real) / quad.real < tol
+    plan.close()

@@ -1,0 +1,129 @@
+"""Pin the CPU oracle (and the host-side table builders) to the reference's golden vectors.
+
+The fixtures in tests/golden were produced by running the real reference package
+(tests/golden/make_golden.py).  These tests run without a GPU.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import nfs_oracle as orc
+from paper_2604_09233_b200 import simulate
+from paper_2604_09233_b200.core import Grid, grid_coordinates
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def test_engine8_operators():
+    g = golden("engine8")
+    t, s, sens = g["temporal"], g["spatial"], g["sens"]
+    assert np.allclose(orc.phase_block(t[10:20], s), g["phase_rows"], atol=1e-14)
+    ph = orc.phase_block(t, s)
+    assert rel(orc.apply_E(g["rho"], sens, ph), g["E_rho"]) < 1e-13
+    assert rel(orc.apply_EH(g["sig_rand"], sens, ph), g["EH_sig"]) < 1e-13
+    dense = orc.dense_encoding_matrix(sens, s, t)
+    assert np.allclose(dense, g["dense"], atol=1e-14)
+    # reference test_engine.py:63-77 dense-equivalence properties on the oracle
+    assert np.allclose(orc.apply_E(g["rho"], sens, ph).ravel(order="F"), dense @ g["rho"], atol=1e-10)
+    assert np.allclose(orc.apply_EH(g["sig_rand"], sens, ph),
+                       dense.conj().T @ g["sig_rand"].ravel(order="F"), atol=1e-10)
+
+
+def test_engine8_cg_full_and_split():
+    g = golden("engine8")
+    args = (g["sigma"], g["spatial"], g["temporal"], g["sens"], np.ones(64), 15)
+    rho, log = orc.recon_full(*args)
+    assert rel(rho, g["full_values"]) < 1e-11
+    assert np.allclose(log.residual_norms, g["full_res"], rtol=1e-9)
+    assert np.allclose(log.solution_norms, g["full_sol"], rtol=1e-11)
+    rho_s, log_s = orc.recon_split(*args, block_starts=g["starts"])
+    assert rel(rho_s, g["split_values"]) < 1e-11
+    assert np.allclose(log_s.residual_norms, g["split_res"], rtol=1e-9)
+    assert np.allclose(rho_s, rho, atol=1e-10)
+
+
+def test_oracle_equivalence_instances():
+    g = golden("oracle_eq")
+    for i in range(4):
+        ph = orc.phase_block(g[f"temporal_{i}"], g[f"spatial_{i}"])
+        assert rel(orc.apply_E(g[f"p_{i}"], g[f"sens_{i}"], ph), g[f"E_{i}"]) < 1e-12
+        assert rel(orc.apply_EH(g[f"sigma_{i}"], g[f"sens_{i}"], ph), g[f"EH_{i}"]) < 1e-12
+
+
+def test_cartesian_exact_recovery_early_stop():
+    g = golden("cartesian8")
+    grid = Grid((8, 8, 1), (0.08, 0.08, 0.002))
+    spatial = np.vstack([np.zeros(64), grid_coordinates(grid)[:, :2].T])
+    rho, log = orc.recon_full(g["sigma"], spatial, g["temporal"], np.ones((64, 1), complex),
+                              np.ones(64), 10)
+    assert len(log.residual_norms) == len(g["res"]) < 10
+    assert rel(rho, g["values"]) < 1e-12
+    assert rel(rho, g["rho_true"]) < 1e-12
+
+
+def test_small3d_full_and_split():
+    g = golden("small3d")
+    args = (g["sigma"], g["spatial"], g["temporal"], g["sens"], np.ones(g["spatial"].shape[1]), 12)
+    rho, log = orc.recon_full(*args)
+    assert rel(rho, g["values"]) < 1e-10
+    assert np.allclose(log.residual_norms, g["res"], rtol=1e-8)
+    rho_s, _ = orc.recon_split(*args, block_starts=g["starts"])
+    assert rel(rho_s, g["split_values"]) < 1e-10
+
+
+def _digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_config_a_generators_match_reference():
+    g = golden("config_a")
+    prob = simulate.make_problem("A")
+    # bit-identical on the build container; tolerant elsewhere (libm differences)
+    assert np.allclose(prob.spatial[:, ::97], g["spatial_rows"], rtol=1e-14, atol=0)
+    assert np.allclose(prob.temporal[::1021], g["temporal_rows"], rtol=1e-14, atol=1e-300)
+    assert np.allclose(prob.sens[::131], g["sens_rows"], rtol=1e-13, atol=1e-15)
+    assert np.allclose(prob.rho_true, g["rho_true"], rtol=1e-14)
+    pm = simulate.make_problem("A_mask")
+    assert np.array_equal(pm.mask_r, g["support"])
+    assert np.allclose(pm.intensity, g["intensity"], rtol=1e-14)
+
+
+def test_config_a_oracle_recon():
+    g = golden("config_a")
+    prob = simulate.make_problem("A")
+    rho, log = orc.recon_full(g["sigma"], prob.spatial, prob.temporal, prob.sens,
+                              prob.intensity, 20)
+    assert rel(rho, g["values"]) < 1e-9
+    assert np.allclose(log.residual_norms, g["res"], rtol=1e-7)
+    pm = simulate.make_problem("A_mask")
+    rho_m, log_m = orc.recon_full(g["sigma"], pm.spatial, pm.temporal, pm.sens, pm.intensity, 20)
+    full = orc.finalize(rho_m, pm.intensity, pm.mask_r, g["kfilter"], pm.grid.dims)
+    assert rel(full, g["values_mask"]) < 1e-9
+    assert np.all(full[~pm.mask_r] != 0) or True  # the k filter spreads energy; no claim
+
+
+def test_config_b_generators_and_rows():
+    g = golden("config_b_rows")
+    prob = simulate.make_problem("B")
+    assert prob.spatial.shape == (16, int(g["n_vox"]))
+    assert np.array_equal(prob.mask_r, g["mask"])
+    assert np.allclose(prob.spatial[:, ::509], g["spatial_cols"], rtol=1e-13, atol=1e-300)
+    rows = g["rows"]
+    assert np.allclose(prob.temporal[rows], g["temporal_rows"], rtol=1e-13, atol=1e-300)
+    s_eff = prob.sens * prob.intensity[:, None]
+    assert np.allclose(s_eff[::509], g["sens_rows"], rtol=1e-13, atol=1e-300)
+    ph = orc.phase_block(prob.temporal[rows], prob.spatial)
+    rho_p = prob.rho_true / prob.intensity
+    assert rel(orc.apply_E(rho_p, s_eff, ph), g["E_rows"]) < 1e-11
+    assert rel(orc.apply_EH(g["sig"], s_eff, ph), g["EH_rows"]) < 1e-11
+
+
+@pytest.mark.parametrize("n,v,b", [(1000, 50, 50 * 16 * 64), (5, 100, 1), (100, 10, 10**9)])
+def test_block_starts(n, v, b):
+    s = orc.choose_block_starts(n, v, b)
+    assert s[0] == 0 and s[-1] == n and np.all(np.diff(s) > 0)
