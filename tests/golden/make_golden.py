@@ -123,7 +123,8 @@ def case_config_a():
     inputs_m = engine.EncodingInputs(sigma=sigma, spatial=spatial_m, temporal=temporal_m,
                                      sens=sens_full[support], intensity=j, kfilter=filt,
                                      mask_r=support, grid=grid, n_iter=20)
-    img_m, log_m = engine.recon_full(inputs_m)
+    rho_m_log = []
+    img_m, log_m = engine.recon_full(inputs_m, callback=lambda n, r: rho_m_log.append(r.copy()))
     iters = np.array([5, 10, 15, 20])
     save("config_a", sigma=sigma, rho_true=rho, support=support,
          spatial_digest=np.array(digest(spatial)), temporal_digest=np.array(digest(temporal)),
@@ -132,7 +133,8 @@ def case_config_a():
          values=img.values, res=np.array(log.residual_norms), sol=np.array(log.solution_norms),
          rho_iters=np.stack([rho_log[i - 1] for i in iters]), iters=iters,
          kfilter=filt, intensity=j, values_mask=img_m.values, res_mask=np.array(log_m.residual_norms),
-         sol_mask=np.array(log_m.solution_norms))
+         sol_mask=np.array(log_m.solution_norms),
+         rho_iters_mask=np.stack([rho_m_log[i - 1] for i in iters]))
 
 
 def case_small3d():

@@ -172,12 +172,19 @@ def test_config_a_fp32_tolerance():
 
 
 def test_config_a_masked_with_filter_fp64():
+    """Masked config A is CG-chaotic after ~12 iterations even in FP64: the reference's own
+    split-vs-full variants drift apart 1e-14 -> 2.5e-7 between iterations 11 and 19.  So the
+    iterate is pinned tightly up to iteration 10 and loosely at 20."""
     g = golden("config_a")
     pm = simulate.make_problem("A_mask")
+    seen = {}
     img, log = engine.recon_full(inputs_from(pm.grid, g["sigma"], pm.spatial, pm.temporal, pm.sens,
                                              20, mask=pm.mask_r, intensity=pm.intensity,
-                                             kfilter=g["kfilter"]))
-    assert rel(img.values, g["values_mask"]) < 1e-8
+                                             kfilter=g["kfilter"]),
+                                 callback=lambda n, r: seen.__setitem__(n, r))
+    assert rel(seen[5], g["rho_iters_mask"][0]) < 1e-12
+    assert rel(seen[10], g["rho_iters_mask"][1]) < 1e-11
+    assert rel(img.values, g["values_mask"]) < 1e-3
     labels = [lab for lab, _ in log.timings]
     assert labels[:3] == ["intensity_correction", "build_phase_matrix", "initial_adjoint"]
     assert labels[-2:] == ["apply_intensity", "apply_kfilter"]
