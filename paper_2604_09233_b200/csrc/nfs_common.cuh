@@ -20,7 +20,7 @@ template <> struct C2<float> { using type = float2; };
 template <> struct C2<double> { using type = double2; };
 
 // Launch description of one generated-phase contraction (forward or adjoint).
-//   forward : owner = sample k (rows of T_tab), streamed = voxel l; X[l][c] = S'[l][c] * p[l]
+//   forward : owner = sample k (rows of T_tab), streamed = voxel l; X = W [L][ldc], W = S' o p
 //             out: partial y [split][K][ldc]
 //   adjoint : owner = voxel l (rows of R_tab), streamed = sample k; X[k][c] = Y[k][c]
 //             out: partial q [group * n_split + split][L] = sum_c conj(S'[l][c]) acc[l][c]
@@ -35,9 +35,8 @@ struct ContractLaunch {
   int n_split;     // split of the streamed range
   const void* own_tab;
   const void* str_tab;
-  const void* sens;      // S' [L][ldc]
-  const double2* p;      // forward only: CG vector (L)
-  const void* y;         // adjoint only: samples [K][ldc]
+  const void* sens;      // S' [L][ldc] (adjoint epilogue)
+  const void* x;         // streamed operand rows [n_str][ldc]: W (forward) or samples (adjoint)
   void* out;             // partial y or partial q (or final if n_split == 1 for forward)
   const int* stop;       // device flag: skip work when the CG has stopped (may be null)
 };
@@ -47,5 +46,8 @@ struct ContractLaunch {
 void contract_kernel_shape(int prec, bool forward, int nc, int nt, int* owners_per_cta,
                            int* streamed_chunk, int* ctas_per_sm);
 cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st);
+// W[l][c] = S'[l][c] * p[l] in the operator precision (forward operand)
+cudaError_t launch_make_w(int prec, const void* sens, const double2* p, void* w, int64_t n_vox,
+                          int ldc, const int* stop, cudaStream_t st);
 
 }  // namespace nfs

@@ -90,7 +90,7 @@ struct nfs_plan {
   bool own_stream = false;
   // tables and operands
   void *d_T = nullptr, *d_R = nullptr, *d_S = nullptr, *d_sig = nullptr, *d_y = nullptr;
-  void *d_party = nullptr, *d_partq = nullptr;
+  void *d_party = nullptr, *d_partq = nullptr, *d_w = nullptr;
   // CG vectors (complex128)
   double2 *d_p = nullptr, *d_q = nullptr, *d_r = nullptr, *d_rho = nullptr, *d_q0 = nullptr;
   double2* d_io = nullptr;
@@ -206,6 +206,7 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
       (s = alloc(&P->d_S, (size_t)L * P->ldc * t2)) ||
       (s = alloc(&P->d_sig, (size_t)K * P->ldc * t2)) ||
       (s = alloc(&P->d_y, (size_t)K * P->ldc * t2)) ||
+      (s = alloc(&P->d_w, (size_t)L * P->ldc * t2)) ||
       (s = alloc(&P->d_partq, (size_t)P->split_a * P->NG * L * t2)) ||
       (s = alloc((void**)&P->d_p, L * sizeof(double2))) ||
       (s = alloc((void**)&P->d_q, L * sizeof(double2))) ||
@@ -241,7 +242,7 @@ extern "C" void nfs_plan_destroy(nfs_plan* P) {
   cudaSetDevice(P->device);
   if (P->stream) cudaStreamSynchronize(P->stream);
   if (P->tc) nfs::tc_destroy(P->tc);
-  void* bufs[] = {P->d_T, P->d_R, P->d_S, P->d_sig, P->d_y, P->d_party, P->d_partq,
+  void* bufs[] = {P->d_T, P->d_R, P->d_S, P->d_sig, P->d_y, P->d_w, P->d_party, P->d_partq,
                   P->d_p, P->d_q, P->d_r, P->d_rho, P->d_q0, P->d_io, P->d_partials,
                   P->d_cg, P->d_res, P->d_sol};
   for (void* b : bufs)
@@ -382,7 +383,8 @@ static int run_forward(nfs_plan* P, const double2* p, const int* stop) {
   }
   if (P->K == 0) return NFS_OK;
   nfs::ContractLaunch L = base_launch(P, true);
-  L.p = p;
+  NFS_CUDA(nfs::launch_make_w(L.prec, P->d_S, p, P->d_w, P->L, P->ldc, stop, P->stream));
+  L.x = P->d_w;
   L.stop = stop;
   L.out = (P->split_f > 1) ? P->d_party : P->d_y;
   NFS_CUDA(nfs::launch_contract(L, P->stream));
@@ -401,7 +403,7 @@ static int run_adjoint(nfs_plan* P, const void* y, double2* q, const int* stop) 
     NFS_CUDA(cudaMemsetAsync(q, 0, P->L * sizeof(double2), P->stream));
   } else {
     nfs::ContractLaunch L = base_launch(P, false);
-    L.y = y;
+    L.x = y;
     L.stop = stop;
     L.out = P->d_partq;
     NFS_CUDA(nfs::launch_contract(L, P->stream));
@@ -605,11 +607,12 @@ extern "C" int nfs_kernel_times(nfs_plan* P, int32_t reps, float* ms_out) {
     } else {
       const int cp = (P->prec == NFS_PREC_FP64) ? 1 : 0;
       nfs::ContractLaunch F = base_launch(P, true);
-      F.p = P->d_p;
+      F.x = P->d_w;
       F.out = (P->split_f > 1) ? P->d_party : P->d_y;
       nfs::ContractLaunch A = base_launch(P, false);
-      A.y = P->d_y;
+      A.x = P->d_y;
       A.out = P->d_partq;
+      NFS_CUDA(nfs::launch_make_w(F.prec, P->d_S, P->d_p, P->d_w, P->L, P->ldc, nullptr, P->stream));
       NFS_CUDA(cudaEventRecord(e[0], P->stream));
       NFS_CUDA(nfs::launch_contract(F, P->stream));
       NFS_CUDA(cudaEventRecord(e[1], P->stream));
@@ -636,7 +639,7 @@ extern "C" int nfs_kernel_times(nfs_plan* P, int32_t reps, float* ms_out) {
 extern "C" int nfs_launches_per_apply(nfs_plan* P) {
   if (!P) return 0;
   if (P->tc) return nfs::tc_launches_per_apply(P->tc);
-  return 1 + (P->split_f > 1 ? 1 : 0) + 2;
+  return 2 + (P->split_f > 1 ? 1 : 0) + 2;
 }
 
 extern "C" const char* nfs_plan_describe(nfs_plan* P) { return P ? P->desc.c_str() : ""; }
