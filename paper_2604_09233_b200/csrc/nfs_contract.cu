@@ -67,9 +67,10 @@ constexpr int kBlockF = 128;
 // streamed items per smem chunk; 32 when NC = NT = 32 keeps static smem under 48 KB
 __host__ __device__ constexpr int chunk_f32(int nc, int nt) { return (nc >= 32 && nt >= 32) ? 32 : 64; }
 
+// phase (turns) of PR owner pairs against one streamed table row b
 template <int NT, int PR>
-__device__ __forceinline__ void phase_pairs(const float2 (&own)[PR][NT], const float* __restrict__ b,
-                                            float2 (&cs)[PR], float2 (&sn)[PR]) {
+__device__ __forceinline__ void phase_t(const float2 (&own)[PR][NT], const float* __restrict__ b,
+                                        float2 (&t)[PR]) {
   float bv[NT];
 #pragma unroll
   for (int p = 0; p < NT; p += 4) {
@@ -79,11 +80,19 @@ __device__ __forceinline__ void phase_pairs(const float2 (&own)[PR][NT], const f
 #pragma unroll
   for (int pr = 0; pr < PR; ++pr) {
     // identical IEEE op sequence to phase_turns_generic<float>: mul, then fma p = 1..NT-1
-    float2 t = __fmul2_rn(own[pr][0], make_float2(bv[0], bv[0]));
+    float2 x = __fmul2_rn(own[pr][0], make_float2(bv[0], bv[0]));
 #pragma unroll
-    for (int p = 1; p < NT; ++p) t = __ffma2_rn(own[pr][p], make_float2(bv[p], bv[p]), t);
-    turns_sincos_generic(t.x, sn[pr].x, cs[pr].x);
-    turns_sincos_generic(t.y, sn[pr].y, cs[pr].y);
+    for (int p = 1; p < NT; ++p) x = __ffma2_rn(own[pr][p], make_float2(bv[p], bv[p]), x);
+    t[pr] = x;
+  }
+}
+
+template <int PR>
+__device__ __forceinline__ void sincos_pairs(const float2 (&t)[PR], float2 (&cs)[PR], float2 (&sn)[PR]) {
+#pragma unroll
+  for (int pr = 0; pr < PR; ++pr) {
+    turns_sincos_generic(t[pr].x, sn[pr].x, cs[pr].x);
+    turns_sincos_generic(t[pr].y, sn[pr].y, cs[pr].y);
   }
 }
 
@@ -92,7 +101,7 @@ __global__ void __launch_bounds__(kBlockF) contract_f32_kernel(ContractLaunch a)
   constexpr int BLOCK = kBlockF, SC = chunk_f32(NC, NT), RO = ro_f32(NC), PR = RO / 2, OWN_TILE = BLOCK * RO;
   if (a.stop != nullptr && *a.stop) return;
 
-  __shared__ __align__(16) float s_tab[2][(SC + 1) * NT];   // row SC = zero row (pipeline tail)
+  __shared__ __align__(16) float s_tab[2][(SC + 2) * NT];   // rows SC, SC+1 = zero (pipeline tail)
   __shared__ __align__(16) float2 s_x[2][SC * NC];
 
   const int tid = threadIdx.x;
@@ -112,7 +121,7 @@ __global__ void __launch_bounds__(kBlockF) contract_f32_kernel(ContractLaunch a)
   if (n_chunks > 0)
     stage_chunk<float, NC, NT, SC, BLOCK>(s_tab[0], s_x[0], str_tab, xs, a.ldc, c0, s_begin, s_end);
   cp_async_commit();
-  if (tid < NT) { s_tab[0][SC * NT + tid] = 0.f; s_tab[1][SC * NT + tid] = 0.f; }
+  if (tid < 2 * NT) { s_tab[0][SC * NT + tid] = 0.f; s_tab[1][SC * NT + tid] = 0.f; }
 
   // owner tables -> packed registers
   float2 own[PR][NT];
@@ -140,12 +149,19 @@ __global__ void __launch_bounds__(kBlockF) contract_f32_kernel(ContractLaunch a)
     __syncthreads();
     const float* tb = s_tab[buf];
     const float2* xb = s_x[buf];
-    float2 cs[PR], sn[PR];
-    phase_pairs<NT, PR>(own, tb, cs, sn);
+    // 3-stage software pipeline: FMA chain for item si+2, sincos for si+1, MACs for si
+    float2 cs[PR], sn[PR], t1[PR];
+    {
+      float2 t0[PR];
+      phase_t<NT, PR>(own, tb, t0);
+      sincos_pairs<PR>(t0, cs, sn);
+      phase_t<NT, PR>(own, tb + NT, t1);
+    }
 #pragma unroll 1
     for (int si = 0; si < SC; ++si) {
-      float2 ncs[PR], nsn[PR];
-      phase_pairs<NT, PR>(own, tb + (si + 1) * NT, ncs, nsn);   // next item, overlaps the MACs
+      float2 t2[PR], ncs[PR], nsn[PR];
+      sincos_pairs<PR>(t1, ncs, nsn);                        // item si+1 (inputs ready)
+      phase_t<NT, PR>(own, tb + (si + 2) * NT, t2);          // item si+2, overlaps the MACs
       float2 msn[PR];
 #pragma unroll
       for (int pr = 0; pr < PR; ++pr) msn[pr] = make_float2(-sn[pr].x, -sn[pr].y);
@@ -176,7 +192,7 @@ __global__ void __launch_bounds__(kBlockF) contract_f32_kernel(ContractLaunch a)
         }
       }
 #pragma unroll
-      for (int pr = 0; pr < PR; ++pr) { cs[pr] = ncs[pr]; sn[pr] = nsn[pr]; }
+      for (int pr = 0; pr < PR; ++pr) { cs[pr] = ncs[pr]; sn[pr] = nsn[pr]; t1[pr] = t2[pr]; }
     }
     __syncthreads();   // buffer `buf` is refilled by the prefetch two chunks ahead
   }

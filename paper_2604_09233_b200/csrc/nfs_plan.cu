@@ -127,11 +127,19 @@ static int pick_nc(int g) {
 }
 
 static int choose_split(int64_t tiles, int64_t n_str, int chunk, int resident) {
-  // enough CTAs for ~4 waves, but keep >= 8 chunks of streamed work per CTA
-  int64_t want = (4LL * resident + tiles - 1) / std::max<int64_t>(tiles, 1);
-  int64_t cap = std::max<int64_t>(1, n_str / (8LL * chunk));
-  int64_t s = std::min(std::max<int64_t>(want, 1), cap);
-  return (int)std::min<int64_t>(s, 64);
+  // Choose the split of the streamed range so that the CTA count fills whole waves of the
+  // resident slots (148 SMs x CTAs/SM): tail waves idle SMs.  Keep >= 4 chunks per CTA.
+  const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(64, n_str / (4LL * chunk)));
+  int best = 1;
+  double best_eff = -1.0;
+  for (int64_t s = 1; s <= cap; ++s) {
+    const double waves = (double)(tiles * s) / resident;
+    if (waves < 1.0 && s < cap) continue;
+    const double eff = waves / std::ceil(waves);
+    if (eff >= 0.97 && waves >= 2.0) return (int)s;   // smallest split that packs well
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = (int)s; }
+  }
+  return best;
 }
 
 static int ensure_io(nfs_plan* P, size_t n_c128) {
