@@ -179,6 +179,7 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
   P->P1 = n_terms;
   P->NT = nt;
   P->NC = pick_nc(n_coils);
+  if (precision == NFS_PREC_TF32X3) P->NC = std::max(P->NC, nfs::tc_coil_width(n_coils));
   P->NG = (n_coils + P->NC - 1) / P->NC;
   P->ldc = P->NC * P->NG;
   P->esz = (precision == NFS_PREC_FP64) ? 8 : 4;

@@ -10,6 +10,8 @@
 namespace nfs {
 
 struct TcPlan;
+// coil group width of the tensor-core path (8, 16 or 32); the plan pads its coil stride to it
+int tc_coil_width(int G);
 TcPlan* tc_create(int64_t K, int64_t L, int G, int nt, int sms, std::string* why);
 void tc_destroy(TcPlan* t);
 const char* tc_describe(TcPlan* t);

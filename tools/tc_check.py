@@ -1,0 +1,26 @@
+"""Quick tensor-core operator check vs the FP32 CUDA-core path and the oracle (small)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from paper_2604_09233_b200._native import Plan
+from oracle import nfs_oracle as orc
+
+rng = np.random.default_rng(3)
+for (L, K, G, P1) in [(300, 500, 8, 3), (301, 777, 40, 17), (1000, 2000, 32, 16), (129, 33, 3, 5)]:
+    spatial = rng.standard_normal((P1, L)) * 0.5
+    temporal = rng.standard_normal((K, P1)) * 2.0
+    sens = rng.standard_normal((L, G)) + 1j * rng.standard_normal((L, G))
+    p = rng.standard_normal(L) + 1j * rng.standard_normal(L)
+    sig = rng.standard_normal((K, G)) + 1j * rng.standard_normal((K, G))
+    ph = orc.phase_block(temporal, spatial)
+    ref_e = orc.apply_E(p, sens, ph)
+    ref_eh = orc.apply_EH(sig, sens, ph)
+    for prec in ("fp32", "tf32x3"):
+        plan = Plan(K, L, G, P1, prec)
+        plan.set_tables(temporal, spatial)
+        plan.set_sens(sens)
+        e = plan.apply_E(p)
+        eh = plan.apply_EH(sig)
+        print(prec, (L, K, G, P1), "E rel", np.linalg.norm(e - ref_e) / np.linalg.norm(ref_e),
+              "EH rel", np.linalg.norm(eh - ref_eh) / np.linalg.norm(ref_eh), plan.describe()[-80:])
+        plan.close()
