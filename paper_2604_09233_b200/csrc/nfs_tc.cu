@@ -32,9 +32,11 @@ namespace tc {
 
 constexpr int IC = 16;          // streamed items per chunk (K = 32 real per chunk)
 constexpr int KC = 2 * IC;      // real K per chunk
-constexpr int STAGES = 3;
+constexpr int SB = 4;           // shared-memory stages of B (+ table rows)
+constexpr int SA = 2;           // TMEM stages of generated A
+constexpr int SEG = 16;         // chunks accumulated in one TMEM D buffer before it is drained
 constexpr int THREADS = 320;
-constexpr int TMEM_COLS = 256;
+constexpr int TMEM_COLS = 256;  // D0 [0,64) D1 [64,128) A stages [128,256)
 constexpr int A_STAGE_COLS = 2 * KC;   // hi + lo
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -145,15 +147,19 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
   constexpr uint32_t T_STAGE_BYTES = IC * NT * 4;
   if (a.stop != nullptr && *a.stop) return;
 
+  // shared memory: B stages | table stages | FP32 accumulator [N][128] | mbarriers | tmem slot
   extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char* sB = smem;                                         // STAGES x B_STAGE_BYTES
-  float* sT = reinterpret_cast<float*>(smem + STAGES * B_STAGE_BYTES);  // STAGES x T_STAGE_BYTES
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * (B_STAGE_BYTES + T_STAGE_BYTES));
-  uint64_t* full_b = bars;
-  uint64_t* full_a = bars + STAGES;
-  uint64_t* empty = bars + 2 * STAGES;
-  uint64_t* d_full = bars + 3 * STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
+  unsigned char* sB = smem;
+  float* sT = reinterpret_cast<float*>(smem + SB * B_STAGE_BYTES);
+  float* sAcc = reinterpret_cast<float*>(smem + SB * (B_STAGE_BYTES + T_STAGE_BYTES));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + N * 128);
+  uint64_t* full_b = bars;              // [SB] producer -> generators, MMA (tx bytes)
+  uint64_t* empty_b = bars + SB;        // [SB] MMA commit -> producer
+  uint64_t* full_a = empty_b + SB;      // [SA] generators (8 warps) -> MMA
+  uint64_t* empty_a = full_a + SA;      // [SA] MMA commit -> generators
+  uint64_t* dfull = empty_a + SA;       // [2]  MMA commit -> drain warps
+  uint64_t* dempty = dfull + 2;         // [2]  drain warps (4) -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int group = blockIdx.y / a.n_split;
@@ -161,15 +167,13 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
   const int per = (a.n_chunks_total + a.n_split - 1) / a.n_split;
   const int chunk0 = split * per;
   const int n_chunks = max(0, min(a.n_chunks_total, chunk0 + per) - chunk0);
+  const int n_segs = (n_chunks + SEG - 1) / SEG;
   const int64_t own0 = (int64_t)blockIdx.x * 128;
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_b[s], 1);
-      mbar_init(&full_a[s], 8);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(d_full, 1);
+    for (int s = 0; s < SB; ++s) { mbar_init(&full_b[s], 1); mbar_init(&empty_b[s], 1); }
+    for (int s = 0; s < SA; ++s) { mbar_init(&full_a[s], 8); mbar_init(&empty_a[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&dfull[s], 1); mbar_init(&dempty[s], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -177,26 +181,43 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  for (int i = tid; i < N * 128; i += THREADS) sAcc[i] = 0.f;
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t d_tmem = tbase;                      // columns [0, N)
-  const uint32_t a_col0 = 64;                         // A stages at [64, 256)
+  constexpr uint32_t A_COL0 = 128;
 
   if (warp < 8) {
-    // ======================= A generators =======================
+    // ======================= A generators (+ D drain, warps 0-3) =======================
     const int q = warp & 3, h = warp >> 2;
     const int64_t o = own0 + q * 32 + lane;
     float own[NT];
 #pragma unroll
     for (int p = 0; p < NT; ++p) own[p] = (o < a.n_own) ? a.own_tab[o * NT + p] : 0.f;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    int next_drain = 0;
+    // TMEM D buffer of segment d -> smem accumulator (FP32, round-to-nearest adds)
+    auto drain = [&](int d) {
+      const int db = d & 1;
+      mbar_wait(&dfull[db], (d >> 1) & 1);
+      fence_after();
+#pragma unroll
+      for (int cb = 0; cb < N; cb += 16) {
+        uint32_t v[16];
+        tmem_ld16(tbase + lane_addr + db * 64 + cb, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sAcc[(cb + i) * 128 + q * 32 + lane] += __uint_as_float(v[i]);
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dempty[db]);
+    };
     for (int c = 0; c < n_chunks; ++c) {
-      const int s = c % STAGES;
-      const uint32_t ph = (c / STAGES) & 1;
-      mbar_wait(&full_b[s], ph);
-      const float* tb = sT + s * (T_STAGE_BYTES / 4);
+      const int sb = c % SB, sa = c % SA;
+      mbar_wait(&full_b[sb], (c / SB) & 1);
+      const float* tb = sT + sb * (T_STAGE_BYTES / 4);
       uint32_t hi[16], lo[16];
 #pragma unroll
       for (int pp = 0; pp < 4; ++pp) {           // 4 item pairs = 8 items of this half
@@ -225,49 +246,38 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
           lo[pp * 4 + e] = __float_as_uint(tf32_rna(vals[e] - vh));
         }
       }
-      mbar_wait(&empty[s], ph ^ 1);   // MMAs of chunk c - STAGES have drained A stage s
+      mbar_wait(&empty_a[sa], ((c / SA) & 1) ^ 1);   // MMAs of chunk c - SA drained A stage sa
       fence_after();
-      const uint32_t col = a_col0 + s * A_STAGE_COLS + h * 16;
+      const uint32_t col = A_COL0 + sa * (2 * KC) + h * 16;
       tmem_st16(tbase + lane_addr + col, hi);
       tmem_st16(tbase + lane_addr + col + KC, lo);
       tmem_wait_st();
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_a[s]);
+      if (lane == 0) mbar_arrive(&full_a[sa]);
+      // drain segment d half-way through segment d+1 (the MMA is then on the other buffer)
+      if (warp < 4 && next_drain < c / SEG && (c % SEG) >= SEG / 2) drain(next_drain++);
     }
-    // ======================= epilogue (warps 0-3) =======================
     if (warp < 4) {
-      float acc[N];
-      if (n_chunks > 0) {
-        mbar_wait(d_full, 0);
-        fence_after();
-#pragma unroll
-        for (int cb = 0; cb < N; cb += 16) {
-          uint32_t v[16];
-          tmem_ld16(tbase + lane_addr + cb, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) acc[cb + i] = __uint_as_float(v[i]);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < N; ++i) acc[i] = 0.f;
-      }
+      while (next_drain < n_segs) drain(next_drain++);
+      __syncwarp();
       if (o < a.n_own) {
         const int c0 = group * NC;
+        const float* acc = sAcc + q * 32 + lane;   // acc[n * 128]
         if constexpr (FWD) {
           float2* out = a.out + (int64_t)split * a.n_own * a.ldc + o * a.ldc + c0;
 #pragma unroll
-          for (int c = 0; c < NC; ++c) out[c] = make_float2(acc[c], acc[NC + c]);
+          for (int c = 0; c < NC; ++c) out[c] = make_float2(acc[c * 128], acc[(NC + c) * 128]);
         } else {
           float qx = 0.f, qy = 0.f;
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             const float2 sv = a.sens[o * a.ldc + c0 + c];   // conj(S') * acc
-            qx = fmaf(sv.x, acc[c], qx);
-            qx = fmaf(sv.y, acc[NC + c], qx);
-            qy = fmaf(sv.x, acc[NC + c], qy);
-            qy = fmaf(-sv.y, acc[c], qy);
+            const float ar = acc[c * 128], ai = acc[(NC + c) * 128];
+            qx = fmaf(sv.x, ar, qx);
+            qx = fmaf(sv.y, ai, qx);
+            qy = fmaf(sv.x, ai, qy);
+            qy = fmaf(-sv.y, ar, qy);
           }
           a.out[(int64_t)blockIdx.y * a.n_own + o] = make_float2(qx, qy);
         }
@@ -277,15 +287,14 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
     // ======================= bulk-copy producer =======================
     if (lane == 0) {
       for (int c = 0; c < n_chunks; ++c) {
-        const int s = c % STAGES;
-        const uint32_t ph = (c / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
+        const int sb = c % SB;
+        mbar_wait(&empty_b[sb], ((c / SB) & 1) ^ 1);
         const int gc = chunk0 + c;
-        mbar_expect_tx(&full_b[s], B_STAGE_BYTES + T_STAGE_BYTES);
+        mbar_expect_tx(&full_b[sb], B_STAGE_BYTES + T_STAGE_BYTES);
         const unsigned char* bsrc = reinterpret_cast<const unsigned char*>(a.b_img) +
                                     ((size_t)group * a.n_chunks_total + gc) * B_STAGE_BYTES;
-        bulk_g2s(sB + s * B_STAGE_BYTES, bsrc, B_STAGE_BYTES, &full_b[s]);
-        bulk_g2s(sT + s * (T_STAGE_BYTES / 4), a.tab_img + (size_t)gc * (IC * NT), T_STAGE_BYTES, &full_b[s]);
+        bulk_g2s(sB + sb * B_STAGE_BYTES, bsrc, B_STAGE_BYTES, &full_b[sb]);
+        bulk_g2s(sT + sb * (T_STAGE_BYTES / 4), a.tab_img + (size_t)gc * (IC * NT), T_STAGE_BYTES, &full_b[sb]);
       }
     }
   } else {
@@ -294,23 +303,29 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
       constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
       constexpr uint32_t LBO = (N / 8) * 128, SBO = 128;
       for (int c = 0; c < n_chunks; ++c) {
-        const int s = c % STAGES;
-        const uint32_t ph = (c / STAGES) & 1;
-        mbar_wait(&full_b[s], ph);
-        mbar_wait(&full_a[s], ph);
+        const int sb = c % SB, sa = c % SA, seg = c / SEG, db = seg & 1;
+        if (c % SEG == 0) {
+          mbar_wait(&dempty[db], ((seg >> 1) & 1) ^ 1);   // segment seg-2 drained from buffer db
+          fence_after();
+        }
+        mbar_wait(&full_b[sb], (c / SB) & 1);
+        mbar_wait(&full_a[sa], (c / SA) & 1);
         fence_after();
-        const uint32_t bhi = smem_u32(sB + s * B_STAGE_BYTES), blo = bhi + B_IMG_BYTES;
-        const uint32_t ahi = tbase + a_col0 + s * A_STAGE_COLS, alo = ahi + KC;
+        const uint32_t d_tmem = tbase + db * 64;
+        const uint32_t bhi = smem_u32(sB + sb * B_STAGE_BYTES), blo = bhi + B_IMG_BYTES;
+        const uint32_t ahi = tbase + A_COL0 + sa * (2 * KC), alo = ahi + KC;
 #pragma unroll
         for (int t = 0; t < KC / 8; ++t) {
           const uint32_t boff = (uint32_t)(2 * t) * LBO;
-          mma_tf32_ts(d_tmem, ahi + 8 * t, smem_desc(bhi + boff, LBO, SBO), idesc, (c > 0 || t > 0) ? 1u : 0u);
+          const uint32_t acc = (c % SEG != 0 || t > 0) ? 1u : 0u;
+          mma_tf32_ts(d_tmem, ahi + 8 * t, smem_desc(bhi + boff, LBO, SBO), idesc, acc);
           mma_tf32_ts(d_tmem, ahi + 8 * t, smem_desc(blo + boff, LBO, SBO), idesc, 1u);
           mma_tf32_ts(d_tmem, alo + 8 * t, smem_desc(bhi + boff, LBO, SBO), idesc, 1u);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&empty_b[sb]);
+        mma_commit(&empty_a[sa]);
+        if (c % SEG == SEG - 1 || c == n_chunks - 1) mma_commit(&dfull[db]);
       }
-      if (n_chunks > 0) mma_commit(d_full);
     }
   }
   fence_before();
@@ -431,7 +446,7 @@ static void* tc_kernel(int nc, int nt, bool fwd) {
 
 static size_t tc_smem_bytes(int nc, int nt) {
   const size_t b = 2ull * tc::KC * (2 * nc) * 4, t = (size_t)tc::IC * nt * 4;
-  return tc::STAGES * (b + t) + (3 * tc::STAGES + 1) * 8 + 16;
+  return tc::SB * (b + t) + (size_t)(2 * nc) * 128 * 4 + (2 * tc::SB + 2 * tc::SA + 4) * 8 + 16;
 }
 
 static int pick_split(int64_t tiles, int chunks, int resident) {
@@ -459,6 +474,7 @@ TcPlan* tc_create(int64_t K, int64_t L, int G, int nt, int sms, std::string* why
   t->smem = tc_smem_bytes(t->nc, nt);
   // keep two CTAs per SM (TMEM: 2 x 256 columns); pad smem so a third cannot co-reside
   const size_t smem_req = std::max<size_t>(t->smem, 80 * 1024);
+  if (smem_req > 110 * 1024) { *why = "shared memory budget"; delete t; return nullptr; }
   for (int fwd = 0; fwd < 2; ++fwd) {
     void* k = tc_kernel(t->nc, nt, fwd != 0);
     if (!k) { *why = "unsupported term count"; delete t; return nullptr; }
