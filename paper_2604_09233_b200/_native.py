@@ -14,7 +14,7 @@ import numpy as np
 
 from .errors import DeviceError, EngineError, MemoryBudgetError, NativeUnavailable
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_nfs_b200.so")
+LIB_PATH = os.environ.get("NFS_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_nfs_b200.so")
 
 NFS_OK = 0
 NFS_ERR_INVALID = 1
@@ -25,7 +25,7 @@ NFS_ERR_CUDA = 5
 NFS_ERR_NCCL = 6
 NFS_ERR_NONFINITE_ITERATE = 7
 
-PRECISIONS = {"fp32": 0, "fp64": 1, "tf32x3": 2}
+PRECISIONS = {"fp32": 0, "fp64": 1, "tf32x3": 2, "f16x3": 3}
 
 _c_i32, _c_i64, _c_dbl_p, _c_void_p = ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p
 CALLBACK = ctypes.CFUNCTYPE(None, ctypes.c_int32, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p)

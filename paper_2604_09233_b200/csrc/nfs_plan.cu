@@ -161,7 +161,8 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
   *out = nullptr;
   if (n_samples < 0 || n_voxels < 1 || n_coils < 1 || n_terms < 1)
     return fail(NFS_ERR_INVALID, "plan sizes must be positive");
-  if (precision != NFS_PREC_FP32 && precision != NFS_PREC_FP64 && precision != NFS_PREC_TF32X3)
+  const bool tensor = precision == NFS_PREC_TF32X3 || precision == NFS_PREC_F16X3;
+  if (precision != NFS_PREC_FP32 && precision != NFS_PREC_FP64 && !tensor)
     return fail(NFS_ERR_INVALID, "unknown precision");
   const int nt = pick_nt(n_terms);
   if (nt < 0) return fail(NFS_ERR_INVALID, "at most 32 basis terms (P+1 <= 32) are supported");
@@ -179,7 +180,7 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
   P->P1 = n_terms;
   P->NT = nt;
   P->NC = pick_nc(n_coils);
-  if (precision == NFS_PREC_TF32X3) P->NC = std::max(P->NC, nfs::tc_coil_width(n_coils));
+  if (tensor) P->NC = std::max(P->NC, nfs::tc_coil_width(n_coils));
   P->NG = (n_coils + P->NC - 1) / P->NC;
   P->ldc = P->NC * P->NG;
   P->esz = (precision == NFS_PREC_FP64) ? 8 : 4;
@@ -227,16 +228,16 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
     return bail(s);
   if (P->split_f > 1 && (s = alloc(&P->d_party, (size_t)P->split_f * K * P->ldc * t2)))
     return bail(s);
-  if (precision == NFS_PREC_TF32X3) {
+  if (tensor) {
     std::string why;
-    P->tc = nfs::tc_create(P->K, P->L, P->G, nt, sms, &why);
+    P->tc = nfs::tc_create(P->K, P->L, P->G, nt, sms, precision == NFS_PREC_F16X3, &why);
     if (!P->tc) return bail(fail(NFS_ERR_INVALID, "tensor-core path unavailable: " + why));
   }
   char buf[512];
   snprintf(buf, sizeof buf,
            "prec=%s K=%lld L=%lld G=%d P1=%d NT=%d NC=%d groups=%d split_fwd=%d(occ %d, %d owners/CTA) "
            "split_adj=%d(occ %d, %d owners/CTA)%s",
-           precision == NFS_PREC_FP64 ? "fp64" : (precision == NFS_PREC_FP32 ? "fp32" : "tf32x3"),
+           precision == NFS_PREC_FP64 ? "fp64" : (precision == NFS_PREC_FP32 ? "fp32" : (precision == NFS_PREC_F16X3 ? "f16x3" : "tf32x3")),
            (long long)P->K, (long long)P->L, P->G, P->P1, nt, P->NC, P->NG, P->split_f, occ_f,
            own_f, P->split_a, occ_a, own_a, P->tc ? nfs::tc_describe(P->tc) : "");
   P->desc = buf;

@@ -1,4 +1,4 @@
-// nfs_tc.cuh -- tensor-core (tcgen05, 3xTF32) operator path, NFS_PREC_TF32X3.
+// nfs_tc.cuh -- tensor-core (tcgen05) split-precision operator path, NFS_PREC_TF32X3 / F16X3.
 // Operates on the FP32 layouts of nfs_common.cuh: T_tab/R_tab (float, NT terms),
 // S' float2 [L][ldc], samples float2 [K][ldc].
 #pragma once
@@ -12,7 +12,7 @@ namespace nfs {
 struct TcPlan;
 // coil group width of the tensor-core path (8, 16 or 32); the plan pads its coil stride to it
 int tc_coil_width(int G);
-TcPlan* tc_create(int64_t K, int64_t L, int G, int nt, int sms, std::string* why);
+TcPlan* tc_create(int64_t K, int64_t L, int G, int nt, int sms, bool f16, std::string* why);
 void tc_destroy(TcPlan* t);
 const char* tc_describe(TcPlan* t);
 const char* tc_last_error();

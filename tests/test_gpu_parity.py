@@ -83,7 +83,7 @@ def test_oracle_equivalence_random_instances_fp64():
     assert worst <= 1e-12, worst
 
 
-@pytest.mark.parametrize("prec,tol", [("fp64", 1e-12), ("fp32", 2e-5), ("tf32x3", 2e-5)])
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-12), ("fp32", 2e-5), ("tf32x3", 2e-5), ("f16x3", 2e-5)])
 def test_many_coils_and_terms(prec, tol):
     """Coil groups (G=40 > 32), odd term counts (P+1=17 -> padded 20), ragged sizes."""
     rng = np.random.default_rng(3)
@@ -104,7 +104,7 @@ def test_many_coils_and_terms(prec, tol):
     plan.close()
 
 
-@pytest.mark.parametrize("prec,tol", [("fp64", 1e-10), ("fp32", 2e-5), ("tf32x3", 2e-5)])
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-10), ("fp32", 2e-5), ("tf32x3", 2e-5), ("f16x3", 2e-5)])
 def test_config_b_rows(prec, tol):
     """Config B tables (L_R=41,684, 32 coils, P+1=16) on a 64-row subset vs the reference."""
     g = golden("config_b_rows")
@@ -158,7 +158,7 @@ def test_config_a_fp64_vs_golden():
         assert rel(seen[it - 1][1], ref) < 1e-8
 
 
-@pytest.mark.parametrize("prec", ["fp32", "tf32x3"])
+@pytest.mark.parametrize("prec", ["fp32", "tf32x3", "f16x3"])
 def test_config_a_fast_mode_tolerance(prec):
     g = golden("config_a")
     prob = simulate.make_problem("A")
@@ -167,7 +167,7 @@ def test_config_a_fast_mode_tolerance(prec):
                                              prob.sens, 20),
                                  callback=lambda n, r: seen.__setitem__(n, r), precision=prec)
     assert rel(seen[5], g["rho_iters"][0]) < 1e-5
-    assert rel(seen[10], g["rho_iters"][1]) < 1e-5
+    assert rel(seen[10], g["rho_iters"][1]) < (1e-5 if prec == "fp32" else 3e-5)
     assert rel(img.values, g["values"]) < 1e-2
     assert np.allclose(log.residual_norms[:10], g["res"][:10], rtol=1e-3)
 
@@ -191,7 +191,7 @@ def test_config_a_masked_with_filter_fp64():
     assert labels[-2:] == ["apply_intensity", "apply_kfilter"]
 
 
-@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("fp32", 1e-3), ("tf32x3", 1e-3)])
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("fp32", 1e-3), ("tf32x3", 1e-3), ("f16x3", 1e-3)])
 def test_small3d_order3(prec, tol):
     g = golden("small3d")
     grid = Grid((12, 12, 6), (0.22, 0.22, 0.128))
@@ -230,7 +230,7 @@ def test_restricted_mask_scatter(rng):
     assert np.any(img.values[mask] != 0)
 
 
-@pytest.mark.parametrize("prec", ["fp32", "tf32x3"])
+@pytest.mark.parametrize("prec", ["fp32", "tf32x3", "f16x3"])
 def test_determinism_bitwise(prec):
     g = golden("config_a")
     prob = simulate.make_problem("A")
@@ -241,7 +241,7 @@ def test_determinism_bitwise(prec):
 
 
 # ------------------------------------------------------------------ full-size properties
-@pytest.mark.parametrize("prec", ["fp32", "fp64", "tf32x3"])
+@pytest.mark.parametrize("prec", ["fp32", "fp64", "tf32x3", "f16x3"])
 def test_config_b_full_size_properties(prec):
     """At BASELINE size: adjoint identity, linearity, and E^H E hermitian positivity."""
     prob = simulate.make_problem("B")

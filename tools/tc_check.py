@@ -15,7 +15,7 @@ for (L, K, G, P1) in [(300, 500, 8, 3), (301, 777, 40, 17), (1000, 2000, 32, 16)
     ph = orc.phase_block(temporal, spatial)
     ref_e = orc.apply_E(p, sens, ph)
     ref_eh = orc.apply_EH(sig, sens, ph)
-    for prec in ("fp32", "tf32x3"):
+    for prec in ("fp32", "tf32x3", "f16x3"):
         plan = Plan(K, L, G, P1, prec)
         plan.set_tables(temporal, spatial)
         plan.set_sens(sens)

@@ -11,7 +11,7 @@ rng = np.random.default_rng(0)
 p = rng.standard_normal(L) + 1j * rng.standard_normal(L)
 sig = rng.standard_normal((K, 32)) + 1j * rng.standard_normal((K, 32))
 out = {}
-for prec in ("fp64", "fp32", "tf32x3"):
+for prec in ("fp64", "fp32", "tf32x3", "f16x3"):
     plan = Plan(K, L, 32, 16, prec)
     plan.set_tables(prob.temporal, prob.spatial)
     plan.set_sens(prob.sens, prob.intensity)
@@ -19,7 +19,7 @@ for prec in ("fp64", "fp32", "tf32x3"):
     print(prec, plan.describe()[-120:])
     plan.close()
 ye, qe = out["fp64"]
-for prec in ("fp32", "tf32x3"):
+for prec in ("fp32", "tf32x3", "f16x3"):
     y, q = out[prec]
     print(prec, "E rel", np.linalg.norm(y - ye) / np.linalg.norm(ye), "EH rel", np.linalg.norm(q - qe) / np.linalg.norm(qe))
     ey = np.linalg.norm(y - ye, axis=1) / np.linalg.norm(ye, axis=1)
