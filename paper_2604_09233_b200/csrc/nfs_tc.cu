@@ -44,10 +44,12 @@ namespace tc {
 
 constexpr int IC = 16;          // streamed items per chunk (K = 32 real per chunk)
 constexpr int KC = 2 * IC;      // real K per chunk
-constexpr int SB = 4;           // shared-memory stages of B (+ table rows)
 constexpr int SEG = 16;         // chunks accumulated in one TMEM D buffer before it is drained
-constexpr int THREADS = 320;
-constexpr int TMEM_COLS = 256;  // D0 [0,64) D1 [64,128) A stages [128,256)
+constexpr int GPQ = 2;          // generator warps per TMEM lane quadrant (chunk c -> warp c % GPQ)
+constexpr int GEN_WARPS = 4 * GPQ;
+constexpr int THREADS = (GEN_WARPS + 2) * 32;
+constexpr int CTAS_PER_SM = 2;
+constexpr int TMEM_COLS = 512 / CTAS_PER_SM;  // D0 [0,64) D1 [64,128) A stages [128, TMEM_COLS)
 constexpr int A_COL0 = 128;
 
 template <bool F16> struct Kind {
@@ -56,6 +58,7 @@ template <bool F16> struct Kind {
   static constexpr int a_img_cols = KC * ebytes / 4;       // TMEM columns per A image (hi or lo)
   static constexpr int sa = (TMEM_COLS - A_COL0) / (2 * a_img_cols);   // A stages
   static constexpr uint32_t fmt = F16 ? 0u : 2u;           // F16 = 0, TF32 = 2
+  static constexpr int sb = sa;                            // B stages tied to A stages
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -71,6 +74,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
         : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (done) break;
+  }
+}
+// wait for a single-thread role (producer, MMA issuer, drain): let the hardware suspend the
+// warp instead of spinning, so it does not steal issue slots from the generator warps
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\nselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity), "r"(1000000)
         : "memory");
     if (done) break;
   }
@@ -133,7 +149,8 @@ __device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) 
 __device__ __forceinline__ void f16_split2(float x, float y, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x, y);
   const float2 hf = __half22float2(h);
-  const __half2 l = __floats2half2_rn(__fsub_rn(x, hf.x), __fsub_rn(y, hf.y));
+  const float2 r = __fadd2_rn(make_float2(x, y), make_float2(-hf.x, -hf.y));
+  const __half2 l = __floats2half2_rn(r.x, r.y);
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
@@ -145,6 +162,16 @@ __device__ __forceinline__ void turns_sincos_fma(float t, float& s, float& c) {
   const float r = __fsub_rn(__fadd_rn(t, magic), magic);
   const float f = __fsub_rn(t, r);
   __sincosf(f * 6.28318530717958647692f, &s, &c);
+}
+
+// packed range reduction of an item pair (FADD2 / FMUL2 on the FMA pipe), MUFU per item
+__device__ __forceinline__ void turns_sincos_pair(float2 t, float& s0, float& c0, float& s1, float& c1) {
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);
+  const float2 r = __fadd2_rn(__fadd2_rn(t, magic), make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __fadd2_rn(t, make_float2(-r.x, -r.y));
+  const float2 a = __fmul2_rn(f, make_float2(6.28318530717958647692f, 6.28318530717958647692f));
+  __sincosf(a.x, &s0, &c0);
+  __sincosf(a.y, &s1, &c1);
 }
 
 template <int NCOL>
@@ -196,14 +223,16 @@ struct Args {
   float2* out;            // fwd: partial y [split][K][ldc]; adj: partial q [group*split+split][L]
   const int* stop;
   int debug;              // profiling only: bit0 skip A math, bit1 skip MMAs
+  long long* trace;       // profiling only: per-chunk timestamps of CTA (0,0), or null
 };
 
 // ------------------------------------------------------------------ main kernel
 template <int NC, int NT, bool FWD, bool F16>
-__global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
+__global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args a) {
   using K_ = Kind<F16>;
   constexpr int N = 2 * NC;
   constexpr int SA = K_::sa;
+  constexpr int SB = K_::sb;
   constexpr int ACOLS = K_::a_img_cols;                    // columns per A image (hi or lo)
   constexpr uint32_t B_IMG_BYTES = KC * N * K_::ebytes;    // one of hi / lo
   constexpr uint32_t B_STAGE_BYTES = 2 * B_IMG_BYTES;
@@ -218,7 +247,7 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + N * 128);
   uint64_t* full_b = bars;              // [SB] producer -> generators, MMA (tx bytes)
   uint64_t* empty_b = bars + SB;        // [SB] MMA commit -> producer
-  uint64_t* full_a = empty_b + SB;      // [SA] generator warps (8) -> MMA
+  uint64_t* full_a = empty_b + SB;      // [SA] generator warps (one per quadrant) -> MMA
   uint64_t* empty_a = full_a + SA;      // [SA] MMA commit -> generators
   uint64_t* dfull = empty_a + SA;       // [2]  MMA commit -> drain warps
   uint64_t* dempty = dfull + 2;         // [2]  drain warps (4) -> MMA
@@ -235,7 +264,7 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
 
   if (tid == 0) {
     for (int s = 0; s < SB; ++s) { mbar_init(&full_b[s], 1); mbar_init(&empty_b[s], 1); }
-    for (int s = 0; s < SA; ++s) { mbar_init(&full_a[s], 8); mbar_init(&empty_a[s], 1); }
+    for (int s = 0; s < SA; ++s) { mbar_init(&full_a[s], 4); mbar_init(&empty_a[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&dfull[s], 1); mbar_init(&dempty[s], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -250,9 +279,9 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
   fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  if (warp < 8) {
+  if (warp < GEN_WARPS) {
     // ======================= A generators (+ D drain, warps 0-3) =======================
-    const int q = warp & 3, h = warp >> 2;
+    const int q = warp & 3, h = warp >> 2;   // lane quadrant, chunk phase (c % GPQ)
     const int64_t o = own0 + q * 32 + lane;
     float own[NT];
 #pragma unroll
@@ -263,7 +292,7 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
     // TMEM D buffer of segment d -> smem accumulator (FP32 round-to-nearest adds)
     auto drain = [&](int d) {
       const int db = d & 1;
-      mbar_wait(&dfull[db], (d >> 1) & 1);
+      mbar_wait_sleep(&dfull[db], (d >> 1) & 1);
       fence_after();
 #pragma unroll
       for (int cb = 0; cb < N; cb += 16) {
@@ -277,56 +306,65 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&dempty[db]);
     };
-    constexpr int NV = F16 ? 8 : 16;   // TMEM columns per warp per image (8 items x cos/sin)
-    for (int c = 0; c < n_chunks; ++c) {
+    constexpr int NV = F16 ? 8 : 16;   // TMEM columns per image per 8 items (cos/sin)
+    // warp (q, h) owns chunks c = h, h + GPQ, ... for its lane quadrant: the warps of a
+    // quadrant work on different chunks, so their barrier waits do not line up
+    for (int c = h; c < n_chunks; c += GPQ) {
       const int sb = c % SB, sa = c % SA;
       mbar_wait(&full_b[sb], (c / SB) & 1);
       const float* tb = sT + sb * (T_STAGE_BYTES / 4);
-      uint32_t hi[NV], lo[NV];
-      if (a.debug & 1) {
+      const uint32_t col = A_COL0 + sa * (2 * ACOLS);
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        uint32_t hi[NV], lo[NV];
+        if (a.debug & 1) {
 #pragma unroll
-        for (int i = 0; i < NV; ++i) { hi[i] = __float_as_uint(own[i % NT]); lo[i] = 0u; }
-      } else {
+          for (int i = 0; i < NV; ++i) { hi[i] = __float_as_uint(own[i % NT]); lo[i] = 0u; }
+        } else {
 #pragma unroll
-        for (int pp = 0; pp < 4; ++pp) {           // 4 item pairs = 8 items of this half
-          const float* row = tb + (h * 4 + pp) * NT * 2;
-          float2 t;
-          {
-            const float4 v = *reinterpret_cast<const float4*>(row);
-            t = __fmul2_rn(make_float2(own[0], own[0]), make_float2(v.x, v.y));
-            t = __ffma2_rn(make_float2(own[1], own[1]), make_float2(v.z, v.w), t);
-          }
+          for (int pp = 0; pp < 4; ++pp) {           // 4 item pairs = 8 items of this half
+            const float* row = tb + (half * 4 + pp) * NT * 2;
+            float2 t;
+            {
+              const float4 v = *reinterpret_cast<const float4*>(row);
+              t = __fmul2_rn(make_float2(own[0], own[0]), make_float2(v.x, v.y));
+              t = __ffma2_rn(make_float2(own[1], own[1]), make_float2(v.z, v.w), t);
+            }
 #pragma unroll
-          for (int p = 2; p < NT; p += 2) {
-            const float4 v = *reinterpret_cast<const float4*>(row + 2 * p);
-            t = __ffma2_rn(make_float2(own[p], own[p]), make_float2(v.x, v.y), t);
-            t = __ffma2_rn(make_float2(own[p + 1], own[p + 1]), make_float2(v.z, v.w), t);
-          }
-          float s0, c0, s1, c1;
-          turns_sincos_fma(t.x, s0, c0);
-          turns_sincos_fma(t.y, s1, c1);
-          if constexpr (F16) {   // one 32-bit column = (cos, sin) of one item
-            f16_split2(c0, s0, hi[pp * 2 + 0], lo[pp * 2 + 0]);
-            f16_split2(c1, s1, hi[pp * 2 + 1], lo[pp * 2 + 1]);
-          } else {
-            tf32_split(c0, hi[pp * 4 + 0], lo[pp * 4 + 0]);
-            tf32_split(s0, hi[pp * 4 + 1], lo[pp * 4 + 1]);
-            tf32_split(c1, hi[pp * 4 + 2], lo[pp * 4 + 2]);
-            tf32_split(s1, hi[pp * 4 + 3], lo[pp * 4 + 3]);
+            for (int p = 2; p < NT; p += 2) {
+              const float4 v = *reinterpret_cast<const float4*>(row + 2 * p);
+              t = __ffma2_rn(make_float2(own[p], own[p]), make_float2(v.x, v.y), t);
+              t = __ffma2_rn(make_float2(own[p + 1], own[p + 1]), make_float2(v.z, v.w), t);
+            }
+            float s0, c0, s1, c1;
+            turns_sincos_pair(t, s0, c0, s1, c1);
+            if constexpr (F16) {   // one 32-bit column = (cos, sin) of one item
+              f16_split2(c0, s0, hi[pp * 2 + 0], lo[pp * 2 + 0]);
+              f16_split2(c1, s1, hi[pp * 2 + 1], lo[pp * 2 + 1]);
+            } else {
+              tf32_split(c0, hi[pp * 4 + 0], lo[pp * 4 + 0]);
+              tf32_split(s0, hi[pp * 4 + 1], lo[pp * 4 + 1]);
+              tf32_split(c1, hi[pp * 4 + 2], lo[pp * 4 + 2]);
+              tf32_split(s1, hi[pp * 4 + 3], lo[pp * 4 + 3]);
+            }
           }
         }
+        if (half == 0) {
+          mbar_wait(&empty_a[sa], ((c / SA) & 1) ^ 1);   // MMAs of chunk c - SA drained stage sa
+          fence_after();
+        }
+        if (!(a.debug & 4)) {
+          tmem_st<NV>(tbase + lane_addr + col + half * NV, hi);
+          tmem_st<NV>(tbase + lane_addr + col + ACOLS + half * NV, lo);
+        }
       }
-      mbar_wait(&empty_a[sa], ((c / SA) & 1) ^ 1);   // MMAs of chunk c - SA drained A stage sa
-      fence_after();
-      const uint32_t col = A_COL0 + sa * (2 * ACOLS) + h * NV;
-      tmem_st<NV>(tbase + lane_addr + col, hi);
-      tmem_st<NV>(tbase + lane_addr + col + ACOLS, lo);
-      tmem_wait_st();
+      if (!(a.debug & 4)) tmem_wait_st();
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_a[sa]);
+      if (a.trace && lane == 0 && q == 0 && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 1] = clock64();
       // drain segment d half-way through segment d+1 (the MMA is then on the other buffer)
-      if (warp < 4 && next_drain < c / SEG && (c % SEG) >= SEG / 2) drain(next_drain++);
+      if (h == 0 && next_drain < c / SEG && (c % SEG) >= SEG / 2) drain(next_drain++);
     }
     if (warp < 4) {
       while (next_drain < n_segs) drain(next_drain++);
@@ -353,13 +391,15 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
         }
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == GEN_WARPS) {
     // ======================= bulk-copy producer =======================
     if (lane == 0) {
       for (int c = 0; c < n_chunks; ++c) {
         const int sb = c % SB;
-        mbar_wait(&empty_b[sb], ((c / SB) & 1) ^ 1);
+        mbar_wait_sleep(&empty_a[sb], ((c / SB) & 1) ^ 1);
         const int gc = chunk0 + c;
+        if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 0] = clock64();
+        if (a.debug & 8) { mbar_arrive(&full_b[sb]); continue; }
         mbar_expect_tx(&full_b[sb], B_STAGE_BYTES + T_STAGE_BYTES);
         const unsigned char* bsrc = reinterpret_cast<const unsigned char*>(a.b_img) +
                                     ((size_t)group * a.n_chunks_total + gc) * B_STAGE_BYTES;
@@ -378,12 +418,14 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
       for (int c = 0; c < n_chunks; ++c) {
         const int sb = c % SB, sa = c % SA, seg = c / SEG, db = seg & 1;
         if (c % SEG == 0) {
-          mbar_wait(&dempty[db], ((seg >> 1) & 1) ^ 1);   // segment seg-2 drained from buffer db
+          mbar_wait_sleep(&dempty[db], ((seg >> 1) & 1) ^ 1);   // segment seg-2 drained from buffer db
           fence_after();
         }
-        mbar_wait(&full_b[sb], (c / SB) & 1);
+        // every generator warp waited full_b[sb] before arriving on full_a[sa], so full_a
+        // completing implies the staged B chunk is visible (release/acquire chain)
         mbar_wait(&full_a[sa], (c / SA) & 1);
         fence_after();
+        if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 2] = clock64();
         const uint32_t d_tmem = tbase + db * 64;
         const uint32_t bhi = smem_u32(sB + sb * B_STAGE_BYTES), blo = bhi + B_IMG_BYTES;
         const uint32_t ahi = tbase + A_COL0 + sa * (2 * ACOLS), alo = ahi + ACOLS;
@@ -396,8 +438,8 @@ __global__ void __launch_bounds__(THREADS, 2) tc_contract_kernel(Args a) {
           mma_ts<F16>(d_tmem, ahi + COLS_PER_STEP * t, smem_desc(blo + boff, LBO, SBO), idesc, 1u);
           mma_ts<F16>(d_tmem, alo + COLS_PER_STEP * t, smem_desc(bhi + boff, LBO, SBO), idesc, 1u);
         }
-        mma_commit(&empty_b[sb]);
-        mma_commit(&empty_a[sa]);
+        mma_commit(&empty_a[sa]);   // A stage and B stage share the index (SB == SA)
+        if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 3] = clock64();
         if (c % SEG == SEG - 1 || c == n_chunks - 1) mma_commit(&dfull[db]);
       }
     }
@@ -544,6 +586,12 @@ static int g_tc_debug = [] {
   return e ? atoi(e) : 0;
 }();
 
+static long long* g_tc_trace = nullptr;
+extern "C" long long* nfs_tc_trace_enable() {   // profiling hook (not part of the C ABI)
+  if (!g_tc_trace) { cudaMallocManaged(&g_tc_trace, 64 * 4 * sizeof(long long)); }
+  return g_tc_trace;
+}
+
 static int tc_fail(const std::string& m) {
   g_tc_err = m;
   return 1;
@@ -583,8 +631,9 @@ static void* tc_kernel(bool f16, int nc, int nt, bool fwd) {
 static size_t tc_smem_bytes(bool f16, int nc, int nt) {
   const int eb = f16 ? 2 : 4;
   const int sa = f16 ? tc::Kind<true>::sa : tc::Kind<false>::sa;
+  const int sb = f16 ? tc::Kind<true>::sb : tc::Kind<false>::sb;
   const size_t b = 2ull * tc::KC * (2 * nc) * eb, t = (size_t)tc::IC * nt * 4;
-  return tc::SB * (b + t) + (size_t)(2 * nc) * 128 * 4 + (2 * tc::SB + 2 * sa + 4) * 8 + 16;
+  return sb * (b + t) + (size_t)(2 * nc) * 128 * 4 + (2 * sb + 2 * sa + 4) * 8 + 16;
 }
 
 static int pick_split(int64_t tiles, int chunks, int resident) {
@@ -610,9 +659,9 @@ TcPlan* tc_create(int64_t K, int64_t L, int G, int nt, int sms, bool f16, std::s
   t->chunks_f = (int)((L + tc::IC - 1) / tc::IC);
   t->chunks_a = (int)((std::max<int64_t>(K, 1) + tc::IC - 1) / tc::IC);
   t->smem = tc_smem_bytes(f16, t->nc, nt);
-  // two CTAs per SM (TMEM 2 x 256 columns); pad smem so a third cannot co-reside
-  const size_t smem_req = std::max<size_t>(t->smem, 80 * 1024);
-  if (smem_req > 110 * 1024) { *why = "shared memory budget"; delete t; return nullptr; }
+  // CTAS_PER_SM CTAs share the 512 TMEM columns; pad smem so no further CTA can co-reside
+  const size_t smem_req = std::max<size_t>(t->smem, tc::CTAS_PER_SM == 1 ? 120 * 1024 : 80 * 1024);
+  if (smem_req > (tc::CTAS_PER_SM == 1 ? 220 : 110) * 1024) { *why = "shared memory budget"; delete t; return nullptr; }
   for (int fwd = 0; fwd < 2; ++fwd) {
     void* k = tc_kernel(f16, t->nc, nt, fwd != 0);
     if (!k) { *why = "unsupported term count"; delete t; return nullptr; }
@@ -623,7 +672,7 @@ TcPlan* tc_create(int64_t K, int64_t L, int G, int nt, int sms, bool f16, std::s
     }
   }
   t->smem = smem_req;
-  const int resident = sms * 2;
+  const int resident = sms * tc::CTAS_PER_SM;
   const int64_t tiles_f = (std::max<int64_t>(K, 1) + 127) / 128 * t->n_groups;
   const int64_t tiles_a = (L + 127) / 128 * t->n_groups;
   t->split_f = pick_split(tiles_f, t->chunks_f, resident);
@@ -724,6 +773,7 @@ static cudaError_t launch_main(TcPlan* t, bool fwd, const int* stop, cudaStream_
   a.out = fwd ? t->part_y : t->part_q;
   a.stop = stop;
   a.debug = g_tc_debug;
+  a.trace = g_tc_trace;
   if (a.n_own <= 0) return cudaSuccess;
   void* k = tc_kernel(t->f16, t->nc, t->nt, fwd);
   dim3 grid((unsigned)((a.n_own + 127) / 128), (unsigned)(a.n_split * t->n_groups));
