@@ -59,7 +59,8 @@ void nfs_plan_destroy(nfs_plan* plan);
 /* Launch on a caller stream (cudaStream_t as void*); NULL = the plan's own stream. */
 int nfs_plan_set_stream(nfs_plan* plan, void* stream);
 /* Sample-sharded multi-GPU: join an NCCL communicator (128-byte ncclUniqueId). The adjoint
- * image is all-reduced (sum) once per CG iteration.  world == 1 needs no call. */
+ * image is all-reduced (sum) once per CG iteration.  world == 1 needs no call (a 1-rank
+ * communicator is accepted and exercises the same all-reduce path). */
 int nfs_plan_attach_comm(nfs_plan* plan, const void* nccl_unique_id, int32_t rank, int32_t world);
 
 /* Basis tables: temporal rows of this rank (K x P1) and spatial (P1 x L_R). */

@@ -276,8 +276,8 @@ extern "C" int nfs_plan_set_stream(nfs_plan* P, void* stream) {
 
 extern "C" int nfs_plan_attach_comm(nfs_plan* P, const void* uid, int32_t rank, int32_t world) {
   if (!P) return fail(NFS_ERR_INVALID, "null plan");
-  if (world <= 1) { P->world = 1; P->rank = 0; return NFS_OK; }
-  if (!uid || rank < 0 || rank >= world) return fail(NFS_ERR_INVALID, "bad rank/world");
+  if (world <= 1 && !uid) { P->world = 1; P->rank = 0; return NFS_OK; }   // no exchange needed
+  if (!uid || world < 1 || rank < 0 || rank >= world) return fail(NFS_ERR_INVALID, "bad rank/world");
   NcclApi& api = nccl_api();
   if (!api.ok) return fail(NFS_ERR_NCCL, "libnccl.so.2 could not be loaded");
   NFS_CUDA(cudaSetDevice(P->device));
@@ -420,7 +420,7 @@ static int run_adjoint(nfs_plan* P, const void* y, double2* q, const int* stop) 
     NFS_CUDA(nfs::launch_reduce_image(L.prec == NFS_PREC_FP64 ? 1 : 0, P->d_partq, q, P->L,
                                       P->split_a * P->NG, stop, P->stream));
   }
-  if (P->world > 1) {
+  if (P->comm) {   // sample-sharded: sum the adjoint images of all ranks (in place)
     int r = nccl_api().allreduce(q, q, (size_t)P->L * 2, kNcclDouble, kNcclSum, P->comm, P->stream);
     if (r != 0) return fail(NFS_ERR_NCCL, "ncclAllReduce failed");
   }

@@ -264,3 +264,21 @@ def test_config_b_full_size_properties(prec):
     assert quad.real > 0 and abs(quad.imag) / quad.real < tol
     assert abs(quad.real - np.vdot(y, y).real) / quad.real < tol
     plan.close()
+
+
+def test_nccl_allreduce_path_single_rank():
+    """The NCCL all-reduce inside the CG graph (1-rank communicator) leaves results unchanged."""
+    import torch.cuda.nccl as tnccl
+    g = golden("engine8")
+    res = []
+    for comm in (False, True):
+        plan = Plan(90, 64, 3, 3, "fp64")
+        if comm:
+            plan.attach_comm(bytes(tnccl.unique_id()), 0, 1)
+        plan.set_tables(g["temporal"], g["spatial"])
+        plan.set_sens(g["sens"])
+        plan.set_samples(g["sigma"])
+        res.append(plan.cg_solve(15)[0])
+        plan.close()
+    assert np.array_equal(res[0], res[1])
+    assert rel(res[1], g["full_values"]) < 1e-10
