@@ -16,8 +16,10 @@
 //   KIND_F16 : kind::f16, hi/lo are FP16 (B scaled by a power of two per call so its largest
 //              entry is ~2^14); half the TMEM / SMEM bytes and twice the MMA rate of TF32.
 // The TMEM accumulator is double-buffered and drained into an FP32 shared-memory accumulator
-// every SEG chunks: the tensor core's accumulation truncates, which over thousands of MMAs
-// drifted to 1.5e-4 relative error; the periodic drain keeps the result at FP32 level.
+// every SEG chunks: the tensor core's accumulation truncates (biased error ~ steps x 2^-24 of
+// |D|), which over thousands of MMAs drifted to 1.5e-4 relative error; measured on config A
+// (E^H sigma) the error scales with SEG: 2.6e-6 at 16, 1.3e-6 at 8, 6.6e-7 at 4 (FP32 path
+// 1.5e-7).  SEG = 8 costs ~3% over 16.
 //
 // Warp roles (320 threads): warps 0-7 generate A (warp w: TMEM lane quadrant w%4, half w/4
 // of each chunk's items); warps 0-3 also drain D and run the epilogue; warp 8 = bulk-copy
@@ -44,7 +46,10 @@ namespace tc {
 
 constexpr int IC = 16;          // streamed items per chunk (K = 32 real per chunk)
 constexpr int KC = 2 * IC;      // real K per chunk
-constexpr int SEG = 16;         // chunks accumulated in one TMEM D buffer before it is drained
+#ifndef NFS_TC_SEG
+#define NFS_TC_SEG 8
+#endif
+constexpr int SEG = NFS_TC_SEG; // chunks accumulated in one TMEM D buffer before it is drained
 constexpr int GPQ = 2;          // generator warps per TMEM lane quadrant (chunk c -> warp c % GPQ)
 constexpr int GEN_WARPS = 4 * GPQ;
 constexpr int THREADS = (GEN_WARPS + 2) * 32;
@@ -364,7 +369,8 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
       if (lane == 0) mbar_arrive(&full_a[sa]);
       if (a.trace && lane == 0 && q == 0 && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 1] = clock64();
       // drain segment d half-way through segment d+1 (the MMA is then on the other buffer)
-      if (h == 0 && next_drain < c / SEG && (c % SEG) >= SEG / 2) drain(next_drain++);
+      // (after producing chunk c >= (d+1)*SEG + SEG/2; the MMA needs it before chunk (d+2)*SEG)
+      while (h == 0 && next_drain < n_segs && (next_drain + 1) * SEG + SEG / 2 <= c) drain(next_drain++);
     }
     if (warp < 4) {
       while (next_drain < n_segs) drain(next_drain++);
