@@ -244,8 +244,15 @@ def main():
         bound, peak_src = "fp32", ("nominal 148 SM x 128 FP32 lanes x 2 flop x sm_max 1965 MHz "
                                    "(MEASURED_PEAKS.json carries no FP32-pipe figure)")
     achieved = flops_1 / (dom_ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+            traffic = json.load(fh).get(args.precision, {}).get(["forward", "adjoint"][dom])
+    except (OSError, ValueError):
+        pass
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_source": "profiles/r1_traffic.json (ncu --set full, dram read+write bytes per launch)",
                 "kernel": ["contract_forward", "contract_adjoint"][dom],
                 "kernel_ms": dom_ms, "algorithmic_flop_per_launch": flops_1,
                 "peak_source": peak_src,
