@@ -17,6 +17,7 @@
 #include "../../include/nfs_b200.h"
 #include "nfs_common.cuh"
 #include "nfs_tc.cuh"
+#include "nfs_tci.cuh"
 #include "nfs_vec.cuh"
 
 using nfs::CGState;
@@ -103,7 +104,8 @@ struct nfs_plan {
   bool have_tables = false, have_sens = false, have_samples = false;
   nfsNcclComm comm = nullptr;
   int rank = 0, world = 1;
-  nfs::TcPlan* tc = nullptr;            // tensor-core operator state (NFS_PREC_TF32X3)
+  nfs::TcPlan* tc = nullptr;            // tensor-core operator, FP32 phase (NFS_PREC_TF32X3)
+  nfs::TciPlan* tci = nullptr;          // tensor-core operator, exact int8 phase (NFS_PREC_F16X3)
   std::string desc;
 };
 
@@ -180,7 +182,7 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
   P->P1 = n_terms;
   P->NT = nt;
   P->NC = pick_nc(n_coils);
-  if (tensor) P->NC = std::max(P->NC, nfs::tc_coil_width(n_coils));
+  if (tensor) P->NC = std::max(P->NC, nfs::tc_coil_width(n_coils));   // 8 / 16 / 32 (same for tci)
   P->NG = (n_coils + P->NC - 1) / P->NC;
   P->ldc = P->NC * P->NG;
   P->esz = (precision == NFS_PREC_FP64) ? 8 : 4;
@@ -228,10 +230,14 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
     return bail(s);
   if (P->split_f > 1 && (s = alloc(&P->d_party, (size_t)P->split_f * K * P->ldc * t2)))
     return bail(s);
-  if (tensor) {
+  if (precision == NFS_PREC_TF32X3) {
     std::string why;
-    P->tc = nfs::tc_create(P->K, P->L, P->G, nt, sms, precision == NFS_PREC_F16X3, &why);
+    P->tc = nfs::tc_create(P->K, P->L, P->G, nt, sms, false, &why);
     if (!P->tc) return bail(fail(NFS_ERR_INVALID, "tensor-core path unavailable: " + why));
+  } else if (precision == NFS_PREC_F16X3) {
+    std::string why;
+    P->tci = nfs::tci_create(P->K, P->L, P->G, nt, sms, &why);
+    if (!P->tci) return bail(fail(NFS_ERR_INVALID, "tensor-core path unavailable: " + why));
   }
   char buf[512];
   snprintf(buf, sizeof buf,
@@ -239,7 +245,7 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
            "split_adj=%d(occ %d, %d owners/CTA)%s",
            precision == NFS_PREC_FP64 ? "fp64" : (precision == NFS_PREC_FP32 ? "fp32" : (precision == NFS_PREC_F16X3 ? "f16x3" : "tf32x3")),
            (long long)P->K, (long long)P->L, P->G, P->P1, nt, P->NC, P->NG, P->split_f, occ_f,
-           own_f, P->split_a, occ_a, own_a, P->tc ? nfs::tc_describe(P->tc) : "");
+           own_f, P->split_a, occ_a, own_a, P->tc ? nfs::tc_describe(P->tc) : (P->tci ? nfs::tci_describe(P->tci) : ""));
   P->desc = buf;
   if (cudaStreamSynchronize(P->stream) != cudaSuccess)
     return bail(fail(NFS_ERR_CUDA, "plan init failed"));
@@ -252,6 +258,7 @@ extern "C" void nfs_plan_destroy(nfs_plan* P) {
   cudaSetDevice(P->device);
   if (P->stream) cudaStreamSynchronize(P->stream);
   if (P->tc) nfs::tc_destroy(P->tc);
+  if (P->tci) nfs::tci_destroy(P->tci);
   void* bufs[] = {P->d_T, P->d_R, P->d_S, P->d_sig, P->d_y, P->d_w, P->d_party, P->d_partq,
                   P->d_p, P->d_q, P->d_r, P->d_rho, P->d_q0, P->d_io, P->d_partials,
                   P->d_cg, P->d_res, P->d_sol};
@@ -316,6 +323,10 @@ extern "C" int nfs_set_tables(nfs_plan* P, const double* temporal, const double*
     int s = nfs::tc_set_tables(P->tc, P->d_T, P->d_R, P->stream);
     if (s) return fail(NFS_ERR_CUDA, "tc tables: " + std::string(nfs::tc_last_error()));
   }
+  if (P->tci) {
+    int s = nfs::tci_set_tables(P->tci, tt.data(), rr.data(), P->stream);
+    if (s) return fail(NFS_ERR_INVALID, "tci tables: " + std::string(nfs::tci_last_error()));
+  }
   return NFS_OK;
 }
 
@@ -342,6 +353,10 @@ extern "C" int nfs_set_sens(nfs_plan* P, const double* sens, const double* inten
   if (P->tc) {
     int s = nfs::tc_set_sens(P->tc, P->d_S, P->ldc, P->stream);
     if (s) return fail(NFS_ERR_CUDA, "tc sens: " + std::string(nfs::tc_last_error()));
+  }
+  if (P->tci) {
+    int s = nfs::tci_set_sens(P->tci, P->d_S, P->ldc, P->stream);
+    if (s) return fail(NFS_ERR_CUDA, "tci sens: " + std::string(nfs::tci_last_error()));
   }
   return NFS_OK;
 }
@@ -391,6 +406,12 @@ static int run_forward(nfs_plan* P, const double2* p, const int* stop) {
     if (s) return fail(NFS_ERR_CUDA, std::string("tc forward: ") + nfs::tc_last_error());
     return NFS_OK;
   }
+  if (P->tci) {
+    int s = nfs::tci_forward_parts(P->tci, p, P->d_y, stop, P->stream, 0);
+    if (!s) s = nfs::tci_forward_parts(P->tci, p, P->d_y, stop, P->stream, 1);
+    if (s) return fail(NFS_ERR_CUDA, std::string("tci forward: ") + nfs::tci_last_error());
+    return NFS_OK;
+  }
   if (P->K == 0) return NFS_OK;
   nfs::ContractLaunch L = base_launch(P, true);
   NFS_CUDA(nfs::launch_make_w(L.prec, P->d_S, p, P->d_w, P->L, P->ldc, stop, P->stream));
@@ -409,6 +430,10 @@ static int run_adjoint(nfs_plan* P, const void* y, double2* q, const int* stop) 
   if (P->tc) {
     int s = nfs::tc_adjoint(P->tc, y, q, stop, P->stream);
     if (s) return fail(NFS_ERR_CUDA, std::string("tc adjoint: ") + nfs::tc_last_error());
+  } else if (P->tci) {
+    int s = nfs::tci_adjoint_parts(P->tci, y, q, stop, P->stream, 0);
+    if (!s) s = nfs::tci_adjoint_parts(P->tci, y, q, stop, P->stream, 1);
+    if (s) return fail(NFS_ERR_CUDA, std::string("tci adjoint: ") + nfs::tci_last_error());
   } else if (P->K == 0) {
     NFS_CUDA(cudaMemsetAsync(q, 0, P->L * sizeof(double2), P->stream));
   } else {
@@ -600,7 +625,17 @@ extern "C" int nfs_kernel_times(nfs_plan* P, int32_t reps, float* ms_out) {
   for (auto& x : e) NFS_CUDA(cudaEventCreate(&x));
   double acc[4] = {0, 0, 0, 0};
   for (int r = 0; r < reps; ++r) {
-    if (P->tc) {
+    if (P->tci) {
+      NFS_CUDA(cudaEventRecord(e[0], P->stream));
+      if (nfs::tci_forward_parts(P->tci, P->d_p, P->d_y, nullptr, P->stream, 0)) return fail(NFS_ERR_CUDA, nfs::tci_last_error());
+      NFS_CUDA(cudaEventRecord(e[1], P->stream));
+      if (nfs::tci_forward_parts(P->tci, P->d_p, P->d_y, nullptr, P->stream, 1)) return fail(NFS_ERR_CUDA, nfs::tci_last_error());
+      NFS_CUDA(cudaEventRecord(e[2], P->stream));
+      if (nfs::tci_adjoint_parts(P->tci, P->d_y, P->d_q, nullptr, P->stream, 0)) return fail(NFS_ERR_CUDA, nfs::tci_last_error());
+      NFS_CUDA(cudaEventRecord(e[3], P->stream));
+      if (nfs::tci_adjoint_parts(P->tci, P->d_y, P->d_q, nullptr, P->stream, 1)) return fail(NFS_ERR_CUDA, nfs::tci_last_error());
+      NFS_CUDA(cudaEventRecord(e[4], P->stream));
+    } else if (P->tc) {
       NFS_CUDA(cudaEventRecord(e[0], P->stream));
       if (nfs::tc_forward_parts(P->tc, P->d_p, P->d_y, nullptr, P->stream, 0))
         return fail(NFS_ERR_CUDA, nfs::tc_last_error());
@@ -649,6 +684,7 @@ extern "C" int nfs_kernel_times(nfs_plan* P, int32_t reps, float* ms_out) {
 extern "C" int nfs_launches_per_apply(nfs_plan* P) {
   if (!P) return 0;
   if (P->tc) return nfs::tc_launches_per_apply(P->tc);
+  if (P->tci) return nfs::tci_launches_per_apply(P->tci);
   return 2 + (P->split_f > 1 ? 1 : 0) + 2;
 }
 
