@@ -1,0 +1,18 @@
+import os, sys, ctypes
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from paper_2604_09233_b200 import _native, simulate
+lib = _native.load_library()
+lib.nfs_tci_trace_enable.restype = ctypes.POINTER(ctypes.c_longlong)
+tr = lib.nfs_tci_trace_enable()
+prob = simulate.make_problem("B")
+K, L = prob.temporal.shape[0], prob.spatial.shape[1]
+plan = _native.Plan(K, L, 32, 16, "f16x3", 0)
+plan.set_tables(prob.temporal, prob.spatial); plan.set_sens(prob.sens, prob.intensity)
+plan.apply_EHE(prob.rho_true)
+plan.kernel_times(1)
+a = np.ctypeslib.as_array(tr, shape=(64, 12)).copy()
+a -= a[0, 0]
+print("chunk phIssued genWaitPh genGotPh genArrA cmmaGo cmmaCommit | ldDone phEmptyArr mathDone emptyAok stDone")
+for c in range(24):
+    print(c, *a[c][:6], '|', *a[c][6:11])
