@@ -15,6 +15,39 @@
 
 namespace nfs {
 
+// Device buffers come from the device's default stream-ordered memory pool with the release
+// threshold raised, so the next plan of a CG solve (or the next recon call) reuses freed
+// memory instead of paying cudaMalloc/cudaFree page-mapping costs (tens to hundreds of ms for
+// the GB-scale partial buffers).  Allocation is made visible to every stream by synchronising
+// the private allocation stream; callers synchronise their own stream before dev_free.
+inline cudaStream_t alloc_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 0;
+  if (!streams[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  }
+  return streams[dev];
+}
+inline cudaError_t dev_alloc(void** p, size_t bytes) {
+  cudaStream_t s = alloc_stream();
+  cudaError_t e = cudaMallocAsync(p, bytes, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return e;
+}
+inline void dev_free(void* p) {
+  if (!p) return;
+  cudaStream_t s = alloc_stream();
+  cudaFreeAsync(p, s);
+}
+
+
 template <typename T> struct C2;
 template <> struct C2<float> { using type = float2; };
 template <> struct C2<double> { using type = double2; };

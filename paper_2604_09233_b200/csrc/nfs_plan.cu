@@ -146,9 +146,12 @@ static int choose_split(int64_t tiles, int64_t n_str, int chunk, int resident) {
 
 static int ensure_io(nfs_plan* P, size_t n_c128) {
   if (P->io_cap >= n_c128) return NFS_OK;
-  if (P->d_io) cudaFree(P->d_io);
+  if (P->d_io) {
+    cudaStreamSynchronize(P->stream);   // the old buffer may still be read by queued work
+    nfs::dev_free(P->d_io);
+  }
   P->d_io = nullptr;
-  NFS_CUDA(cudaMalloc(&P->d_io, n_c128 * sizeof(double2)));
+  NFS_CUDA(nfs::dev_alloc((void**)&P->d_io, n_c128 * sizeof(double2)));
   P->io_cap = n_c128;
   return NFS_OK;
 }
@@ -208,7 +211,7 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
 
   const size_t t2 = t2size(P);
   auto alloc = [&](void** p, size_t bytes) -> int {
-    NFS_CUDA(cudaMalloc(p, std::max<size_t>(bytes, 16)));
+    NFS_CUDA(nfs::dev_alloc(p, std::max<size_t>(bytes, 16)));
     NFS_CUDA(cudaMemsetAsync(*p, 0, std::max<size_t>(bytes, 16), P->stream));
     return NFS_OK;
   };
@@ -263,7 +266,7 @@ extern "C" void nfs_plan_destroy(nfs_plan* P) {
                   P->d_p, P->d_q, P->d_r, P->d_rho, P->d_q0, P->d_io, P->d_partials,
                   P->d_cg, P->d_res, P->d_sol};
   for (void* b : bufs)
-    if (b) cudaFree(b);
+    if (b) nfs::dev_free(b);
   if (P->comm && nccl_api().ok) nccl_api().destroy(P->comm);
   if (P->own_stream && P->stream) cudaStreamDestroy(P->stream);
   delete P;
@@ -501,12 +504,12 @@ extern "C" int nfs_phase_rows(nfs_plan* P, int64_t lo, int64_t hi, double* out) 
   NFS_CUDA(cudaSetDevice(P->device));
   const size_t n = (size_t)(hi - lo) * P->L;
   double2* d = nullptr;
-  NFS_CUDA(cudaMalloc(&d, n * sizeof(double2)));
+  NFS_CUDA(nfs::dev_alloc((void**)&d, n * sizeof(double2)));
   cudaError_t e = nfs::launch_phase_rows(P->prec == NFS_PREC_FP64 ? 1 : 0, P->NT, P->d_T, P->d_R,
                                          lo, hi - lo, P->L, d, P->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, n * sizeof(double2), cudaMemcpyDeviceToHost, P->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
-  cudaFree(d);
+  nfs::dev_free(d);
   if (e != cudaSuccess) return fail(NFS_ERR_CUDA, std::string("phase rows: ") + cudaGetErrorString(e));
   return NFS_OK;
 }
@@ -528,11 +531,12 @@ extern "C" int nfs_cg_solve(nfs_plan* P, int32_t n_iter, nfs_iter_callback cb, v
   if (n_iter < 0) return fail(NFS_ERR_INVALID, "negative iteration count");
   if (n_done) *n_done = 0;
   if (n_iter > P->log_cap) {
-    if (P->d_res) cudaFree(P->d_res);
-    if (P->d_sol) cudaFree(P->d_sol);
+    cudaStreamSynchronize(P->stream);
+    if (P->d_res) nfs::dev_free(P->d_res);
+    if (P->d_sol) nfs::dev_free(P->d_sol);
     P->d_res = P->d_sol = nullptr;
-    NFS_CUDA(cudaMalloc(&P->d_res, std::max(n_iter, 1) * sizeof(double)));
-    NFS_CUDA(cudaMalloc(&P->d_sol, std::max(n_iter, 1) * sizeof(double)));
+    NFS_CUDA(nfs::dev_alloc((void**)&P->d_res, std::max(n_iter, 1) * sizeof(double)));
+    NFS_CUDA(nfs::dev_alloc((void**)&P->d_sol, std::max(n_iter, 1) * sizeof(double)));
     P->log_cap = n_iter;
   }
   std::vector<cudaEvent_t> ev(n_iter + 2);

@@ -684,7 +684,7 @@ TcPlan* tc_create(int64_t K, int64_t L, int G, int nt, int sms, bool f16, std::s
   t->split_f = pick_split(tiles_f, t->chunks_f, resident);
   t->split_a = pick_split(tiles_a, t->chunks_a, resident);
   const size_t img_chunk = 2ull * tc::KC * (2 * t->nc) * (f16 ? 2 : 4);   // bytes per chunk (hi + lo)
-  auto al = [&](void** p, size_t bytes) { return cudaMalloc(p, std::max<size_t>(bytes, 256)) == cudaSuccess; };
+  auto al = [&](void** p, size_t bytes) { return nfs::dev_alloc(p, std::max<size_t>(bytes, 256)) == cudaSuccess; };
   bool ok = al(&t->img_f, img_chunk * t->chunks_f * t->n_groups) &&
             al(&t->img_a, img_chunk * t->chunks_a * t->n_groups) &&
             al((void**)&t->tab_f, (size_t)t->chunks_f * tc::IC * nt * 4) &&
@@ -707,7 +707,7 @@ void tc_destroy(TcPlan* t) {
   if (!t) return;
   void* bufs[] = {t->img_f, t->img_a, t->tab_f, t->tab_a, t->part_y, t->part_q, t->d_amax, t->d_scale};
   for (void* b : bufs)
-    if (b) cudaFree(b);
+    if (b) nfs::dev_free(b);
   delete t;
 }
 
