@@ -126,20 +126,23 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
                                        uint32_t accumulate) {
   if constexpr (F16)
     asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+        "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|q, 0xffffffff;\n"
+        "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
   else
     asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+        "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|q, 0xffffffff;\n"
+        "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// issued by a converged warp: elect.sync inside the asm avoids ptxas' per-MMA waterfall loop
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+  asm volatile(
+      "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_u32(bar))
+      : "memory");
 }
 
 // TF32 split: hi = round-half-away TF32 (finite x), lo = x - hi exact; the MMA truncates lo's
@@ -414,8 +417,8 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
       }
     }
   } else {
-    // ======================= MMA issuer =======================
-    if (lane == 0) {
+    // ======================= MMA issuer (whole warp, elected issue) =======================
+    {
       constexpr uint32_t idesc =
           (1u << 4) | (K_::fmt << 7) | (K_::fmt << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
       constexpr uint32_t LBO = (N / 8) * 128, SBO = 128;
@@ -431,7 +434,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
         // completing implies the staged B chunk is visible (release/acquire chain)
         mbar_wait(&full_a[sa], (c / SA) & 1);
         fence_after();
-        if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 2] = clock64();
+        if (a.trace && lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 2] = clock64();
         const uint32_t d_tmem = tbase + db * 64;
         const uint32_t bhi = smem_u32(sB + sb * B_STAGE_BYTES), blo = bhi + B_IMG_BYTES;
         const uint32_t ahi = tbase + A_COL0 + sa * (2 * ACOLS), alo = ahi + ACOLS;
@@ -445,7 +448,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
           mma_ts<F16>(d_tmem, alo + COLS_PER_STEP * t, smem_desc(bhi + boff, LBO, SBO), idesc, 1u);
         }
         mma_commit(&empty_a[sa]);   // A stage and B stage share the index (SB == SA)
-        if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 3] = clock64();
+        if (a.trace && lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 3] = clock64();
         if (c % SEG == SEG - 1 || c == n_chunks - 1) mma_commit(&dfull[db]);
       }
     }
