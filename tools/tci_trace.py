@@ -13,6 +13,6 @@ plan.apply_EHE(prob.rho_true)
 plan.kernel_times(1)
 a = np.ctypeslib.as_array(tr, shape=(64, 12)).copy()
 a -= a[0, 0]
-print("chunk phIssued genWaitPh genGotPh genArrA cmmaGo cmmaCommit | ldDone phEmptyArr mathDone emptyAok stDone")
+print("chunk phIssued itStart emptyAok genArrA cmmaGo cmmaCommit | pfWait pfGot mathEnd phEmptyArr")
 for c in range(24):
-    print(c, *a[c][:6], '|', *a[c][6:11])
+    print(c, *a[c][:6], '|', *a[c][6:10])
