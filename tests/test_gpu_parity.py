@@ -282,3 +282,33 @@ def test_nccl_allreduce_path_single_rank():
         plan.close()
     assert np.array_equal(res[0], res[1])
     assert rel(res[1], g["full_values"]) < 1e-10
+
+
+# ------------------------------------------------------------------ config D (f2: device synthesis)
+@pytest.fixture(scope="module")
+def problem_d():
+    return simulate.make_problem("D")
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-10), ("f16x3", 2e-5)])
+def test_config_d_device_synthesis_rows(problem_d, prec, tol):
+    """sigma = E rho synthesised on the GPU at full config-D size (L_R=532,872
+    voxels, K=299,648 samples, 32 coils, P+1=16) agrees on a random row subset with the
+    sample-by-sample loop oracle (nfs/simulate.py:219-244); the CPU cannot synthesise all rows."""
+    prob = problem_d
+    K, L = prob.temporal.shape[0], prob.spatial.shape[1]
+    plan = Plan(K, L, 32, 16, prec)
+    plan.set_tables(prob.temporal, prob.spatial)
+    plan.set_sens(prob.sens, prob.intensity)
+    y = plan.apply_E(prob.rho_true / prob.intensity)          # S' (rho / j) = S rho
+    rows = np.sort(np.random.default_rng(5).choice(K, 12, replace=False))
+    ref = orc.forward_signal(prob.rho_true, prob.sens, prob.spatial, prob.temporal[rows])
+    assert rel(y[rows], ref) < tol
+    # adjoint identity at full size (the operator pair CG uses)
+    rng = np.random.default_rng(1)
+    sig = (rng.standard_normal((K, 32)) + 1j * rng.standard_normal((K, 32))) * 1e-3
+    q = plan.apply_EH(sig)
+    p = prob.rho_true
+    lhs, rhs = np.vdot(sig, plan.apply_E(p)), np.vdot(q, p)
+    assert abs(lhs - rhs) / abs(lhs) < (1e-11 if prec == "fp64" else 1e-5)
+    plan.close()
