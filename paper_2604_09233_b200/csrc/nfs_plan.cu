@@ -328,7 +328,16 @@ extern "C" int nfs_set_tables(nfs_plan* P, const double* temporal, const double*
   }
   if (P->tci) {
     int s = nfs::tci_set_tables(P->tci, tt.data(), rr.data(), P->stream);
-    if (s) return fail(NFS_ERR_INVALID, "tci tables: " + std::string(nfs::tci_last_error()));
+    if (s == 2) {
+      // the exact int8 phase cannot represent this basis (some |t'_p r_p| > 2^12 turns): run
+      // the plan on the FP32 CUDA-core contraction instead (same buffers, same results within
+      // the FP32 tolerance) and say so in the description
+      nfs::tci_destroy(P->tci);
+      P->tci = nullptr;
+      P->desc += " [f16x3 unavailable for this basis (phase range): FP32 CUDA-core contraction]";
+    } else if (s) {
+      return fail(NFS_ERR_INVALID, "tci tables: " + std::string(nfs::tci_last_error()));
+    }
   }
   return NFS_OK;
 }

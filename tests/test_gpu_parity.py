@@ -312,3 +312,25 @@ def test_config_d_device_synthesis_rows(problem_d, prec, tol):
     lhs, rhs = np.vdot(sig, plan.apply_E(p)), np.vdot(q, p)
     assert abs(lhs - rhs) / abs(lhs) < (1e-11 if prec == "fp64" else 1e-5)
     plan.close()
+
+
+def test_f16x3_phase_range_fallback():
+    """A basis whose phase exceeds the exact int8 fixed-point range (|t'_p r_p| > 2^12 turns)
+    runs the f16x3 plan on the FP32 CUDA-core contraction (said so in describe()), agreeing
+    with an fp32 plan."""
+    rng = np.random.default_rng(11)
+    L, K, G, P1 = 200, 300, 8, 3
+    spatial = rng.standard_normal((P1, L))
+    temporal = rng.standard_normal((K, P1)) * 2.0e5          # |phase| up to ~1e5 rad per term
+    sens = rng.standard_normal((L, G)) + 1j * rng.standard_normal((L, G))
+    p = rng.standard_normal(L) + 1j * rng.standard_normal(L)
+    out = {}
+    for prec in ("f16x3", "fp32"):
+        plan = Plan(K, L, G, P1, prec)
+        plan.set_tables(temporal, spatial)
+        plan.set_sens(sens)
+        out[prec] = plan.apply_EHE(p)
+        if prec == "f16x3":
+            assert "FP32 CUDA-core contraction" in plan.describe()
+        plan.close()
+    assert rel(out["f16x3"], out["fp32"]) < 1e-5
