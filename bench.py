@@ -260,6 +260,12 @@ def main():
                                   "adjoint_reduce": kt[3]}}
     if clocks.get("sm_mhz"):
         roofline["frac_at_observed_clock"] = achieved / (peak * clocks["sm_mhz"] / 1965.0)
+    # the phasor e^{i phi} costs 2 MUFU ops (sin, cos) per pair in every mode: the SFU floor
+    # (16 MUFU lane-ops / clk / SM, tools/ubench/mufu_rate.cu) is the binding resource of the
+    # tensor-core modes
+    if args.precision != "fp64":
+        mufu_peak = 148 * 16 * 1.965e9
+        roofline["mufu_frac"] = 2.0 * float(k_loc) * L / (dom_ms * 1e-3) / mufu_peak
     if args.precision in ("f16x3", "tf32x3"):
         # the split MMA executes 3 products on the real-ified operands: 3 x 2 x (2 x 2G) per pair
         executed = float(k_loc) * L * 3 * 2 * 2 * (2 * G) * 2 / 2
