@@ -65,6 +65,13 @@ int nfs_plan_attach_comm(nfs_plan* plan, const void* nccl_unique_id, int32_t ran
 
 /* Basis tables: temporal rows of this rank (K x P1) and spatial (P1 x L_R). */
 int nfs_set_tables(nfs_plan* plan, const double* temporal, const double* spatial);
+/* Same, with the spatial table evaluated ON THE DEVICE from the masked voxels' linear grid
+ * indices (ix + nx (iy + ny iz)), their B0 (rad/s), the grid extents dims[3], FOV fov[3] (m)
+ * and the harmonic order 1..3 -- replaces engine.build_bases (nfs/engine.py:252-280) +
+ * solid_harmonics (nfs/simulate.py:26-59) + grid_coordinates (nfs/core.py:102-113); the table
+ * is bit-identical to the host build.  P1 must equal 1 + the order's harmonic count. */
+int nfs_set_tables_grid(nfs_plan* plan, const double* temporal, const int64_t* vox_index,
+                        const double* b0_masked, const int32_t* dims, const double* fov, int32_t order);
 /* Sensitivities (L_R x G complex) and optional intensity correction j (L_R) -> S' = S o j
  * (nfs/engine.py:143).  intensity == NULL means j = 1 (apply_E / apply_EH semantics). */
 int nfs_set_sens(nfs_plan* plan, const double* sens, const double* intensity);

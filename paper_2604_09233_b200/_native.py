@@ -37,6 +37,8 @@ SIGNATURES = {
     "nfs_plan_set_stream": (_c_i32, [_c_void_p, _c_void_p]),
     "nfs_plan_attach_comm": (_c_i32, [_c_void_p, ctypes.c_char_p, _c_i32, _c_i32]),
     "nfs_set_tables": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
+    "nfs_set_tables_grid": (_c_i32, [_c_void_p, _c_dbl_p, ctypes.POINTER(_c_i64), _c_dbl_p,
+                                     ctypes.POINTER(_c_i32), _c_dbl_p, _c_i32]),
     "nfs_set_sens": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
     "nfs_set_samples": (_c_i32, [_c_void_p, _c_dbl_p]),
     "nfs_apply_E": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
@@ -141,6 +143,17 @@ class Plan:
         t = np.ascontiguousarray(temporal, dtype=np.float64).reshape(k, p1)
         s = np.ascontiguousarray(spatial, dtype=np.float64).reshape(p1, l)
         _check(self._lib.nfs_set_tables(self._h, _dp(t), _dp(s)))
+
+    def set_tables_grid(self, temporal, vox_index, b0_masked, dims, fov, order):
+        """Spatial table evaluated on the device; see nfs_set_tables_grid."""
+        k, l, _, p1 = self.shape
+        t = np.ascontiguousarray(temporal, dtype=np.float64).reshape(k, p1)
+        v = np.ascontiguousarray(vox_index, dtype=np.int64).reshape(l)
+        b = np.ascontiguousarray(b0_masked, dtype=np.float64).reshape(l)
+        d = np.ascontiguousarray(dims, dtype=np.int32).reshape(3)
+        f = np.ascontiguousarray(fov, dtype=np.float64).reshape(3)
+        _check(self._lib.nfs_set_tables_grid(self._h, _dp(t), v.ctypes.data_as(ctypes.POINTER(_c_i64)), _dp(b),
+                                             d.ctypes.data_as(ctypes.POINTER(_c_i32)), _dp(f), int(order)))
 
     def set_sens(self, sens, intensity=None):
         _, l, g, _ = self.shape

@@ -1,0 +1,101 @@
+// nfs_bases.cu -- spatial basis table evaluated on the device from voxel indices.
+//
+// R[l, 0] = B0 (rad/s) of masked voxel l, R[l, 1..] = the zero-Laplacian solid harmonics of its
+// grid coordinates (order 1 / 2 / 3: 2-or-3 / 8 / 15 terms), in the plan's [L_R][NT] FP64 table
+// layout.  Restates engine.build_bases (nfs/engine.py:252-280), solid_harmonics
+// (nfs/simulate.py:26-59) and grid_coordinates (nfs/core.py:102-113) with explicitly rounded
+// IEEE operations in numpy's evaluation order, so the table is bit-identical to the host build.
+// Only the voxel index (8 B) and B0 (8 B) cross PCIe per voxel instead of P+1 doubles.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nfs_bases.cuh"
+
+namespace nfs {
+
+__device__ __forceinline__ double axis_coord(int64_t m, int n, double fov) {
+  const double pitch = __ddiv_rn(fov, (double)n);                   // fov / n
+  const double off = __dsub_rn((double)m, __ddiv_rn((double)(n - 1), 2.0));   // m - (n-1)/2
+  return __dmul_rn(pitch, off);
+}
+
+__global__ void spatial_from_grid_kernel(const int64_t* __restrict__ vox, const double* __restrict__ b0,
+                                         int64_t L, int nt, int nx, int ny, int nz, double fx, double fy,
+                                         double fz, int ndim, int order, double* __restrict__ rr) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L; l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t idx = vox[l];
+    const int64_t ix = idx % nx, iy = (idx / nx) % ny, iz = idx / ((int64_t)nx * ny);
+    const double x = axis_coord(ix, nx, fx), y = axis_coord(iy, ny, fy), z = axis_coord(iz, nz, fz);
+    double* r = rr + l * nt;
+    int p = 0;
+    r[p++] = b0[l];
+    r[p++] = x;
+    r[p++] = y;
+    if (!(ndim == 2 && order == 1)) r[p++] = z;
+    const double x2 = __dmul_rn(x, x), y2 = __dmul_rn(y, y), z2 = __dmul_rn(z, z);
+    if (order >= 2) {
+      r[p++] = __dmul_rn(x, y);
+      r[p++] = __dmul_rn(z, y);
+      r[p++] = __dsub_rn(__dsub_rn(__dmul_rn(2.0, z2), x2), y2);           // 2 z^2 - x^2 - y^2
+      r[p++] = __dmul_rn(z, x);
+      r[p++] = __dsub_rn(x2, y2);
+    }
+    if (order >= 3) {
+      r[p++] = __dmul_rn(y, __dsub_rn(__dmul_rn(3.0, x2), y2));                           // y (3x^2 - y^2)
+      r[p++] = __dmul_rn(__dmul_rn(x, y), z);                                              // x y z
+      r[p++] = __dmul_rn(y, __dsub_rn(__dsub_rn(__dmul_rn(4.0, z2), x2), y2));           // y (4z^2 - x^2 - y^2)
+      r[p++] = __dmul_rn(z, __dsub_rn(__dsub_rn(__dmul_rn(2.0, z2), __dmul_rn(3.0, x2)), __dmul_rn(3.0, y2)));
+      r[p++] = __dmul_rn(x, __dsub_rn(__dsub_rn(__dmul_rn(4.0, z2), x2), y2));           // x (4z^2 - x^2 - y^2)
+      r[p++] = __dmul_rn(z, __dsub_rn(x2, y2));                                            // z (x^2 - y^2)
+      r[p++] = __dmul_rn(x, __dsub_rn(x2, __dmul_rn(3.0, y2)));                           // x (x^2 - 3y^2)
+    }
+    for (; p < nt; ++p) r[p] = 0.0;
+  }
+}
+
+// per-column max |v| of a [n][nt] FP64 table (for the fixed-point scales of the int8 phase)
+__global__ void col_absmax_kernel(const double* __restrict__ tab, int64_t n, int nt, unsigned long long* out) {
+  for (int p = 0; p < nt; ++p) {
+    double m = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+      m = fmax(m, fabs(tab[i * nt + p]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&out[p], (unsigned long long)__double_as_longlong(m));   // m >= 0
+  }
+}
+
+__global__ void to_float_kernel(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)in[i];
+}
+
+int harmonic_terms(int order, int ndim) {
+  if (order == 1) return ndim == 2 ? 2 : 3;
+  if (order == 2) return 8;
+  if (order == 3) return 15;
+  return -1;
+}
+
+static int grid_for(int64_t n) { return (int)(n / 256 + 1 < 148 * 8 ? n / 256 + 1 : 148 * 8); }
+
+cudaError_t launch_spatial_from_grid(const int64_t* d_vox, const double* d_b0, int64_t L, int nt, const int* dims,
+                                     const double* fov, int order, double* d_rr, cudaStream_t st) {
+  const int ndim = dims[2] == 1 ? 2 : 3;
+  spatial_from_grid_kernel<<<grid_for(L), 256, 0, st>>>(d_vox, d_b0, L, nt, dims[0], dims[1], dims[2], fov[0], fov[1],
+                                                        fov[2], ndim, order, d_rr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_col_absmax(const double* d_tab, int64_t n, int nt, unsigned long long* d_out, cudaStream_t st) {
+  cudaMemsetAsync(d_out, 0, nt * sizeof(unsigned long long), st);
+  col_absmax_kernel<<<grid_for(n), 256, 0, st>>>(d_tab, n, nt, d_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_float(const double* d_in, float* d_out, int64_t n, cudaStream_t st) {
+  to_float_kernel<<<grid_for(n), 256, 0, st>>>(d_in, d_out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace nfs

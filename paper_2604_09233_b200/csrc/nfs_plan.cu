@@ -18,6 +18,7 @@
 #include "nfs_common.cuh"
 #include "nfs_tc.cuh"
 #include "nfs_tci.cuh"
+#include "nfs_bases.cuh"
 #include "nfs_vec.cuh"
 
 using nfs::CGState;
@@ -339,6 +340,94 @@ extern "C" int nfs_set_tables(nfs_plan* P, const double* temporal, const double*
       return fail(NFS_ERR_INVALID, "tci tables: " + std::string(nfs::tci_last_error()));
     }
   }
+  return NFS_OK;
+}
+
+// Spatial table evaluated on the device from the masked voxel indices: same
+// tables as nfs_set_tables(temporal, build_bases(...)[0]) bit for bit.
+extern "C" int nfs_set_tables_grid(nfs_plan* P, const double* temporal, const int64_t* vox_index,
+                                   const double* b0_masked, const int32_t* dims, const double* fov, int32_t order) {
+  if (!P || (!temporal && P->K > 0) || !vox_index || !b0_masked || !dims || !fov)
+    return fail(NFS_ERR_INVALID, "null argument");
+  if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || !(fov[0] > 0) || !(fov[1] > 0) || !(fov[2] > 0))
+    return fail(NFS_ERR_INVALID, "grid extents and FOV must be positive");
+  const int ndim = dims[2] == 1 ? 2 : 3;
+  const int nh = nfs::harmonic_terms(order, ndim);
+  if (nh < 0) return fail(NFS_ERR_INVALID, "unsupported harmonic order " + std::to_string(order));
+  if (1 + nh != P->P1)
+    return fail(NFS_ERR_INVALID, "order " + std::to_string(order) + " gives " + std::to_string(1 + nh) +
+                                     " basis rows but the plan has " + std::to_string(P->P1));
+  const int64_t nvox = (int64_t)dims[0] * dims[1] * dims[2];
+  for (int64_t l = 0; l < P->L; ++l)
+    if (vox_index[l] < 0 || vox_index[l] >= nvox) return fail(NFS_ERR_INVALID, "voxel index outside the grid");
+  NFS_CUDA(cudaSetDevice(P->device));
+  const int nt = P->NT, p1 = P->P1;
+  const int64_t K = P->K, L = P->L;
+  const double inv2pi = 1.0 / 6.283185307179586476925286766559;
+  std::vector<double> tt((size_t)K * nt, 0.0), amax_t(nt, 0.0), amax_r(nt, 0.0);
+  for (int64_t k = 0; k < K; ++k)
+    for (int p = 0; p < p1; ++p) {
+      tt[(size_t)k * nt + p] = temporal[(size_t)k * p1 + p] * inv2pi;
+      amax_t[p] = std::max(amax_t[p], std::fabs(tt[(size_t)k * nt + p]));
+    }
+  int64_t* d_vox = nullptr;
+  double *d_b0 = nullptr, *d_rr = nullptr, *d_tt = nullptr;
+  unsigned long long* d_max = nullptr;
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(P->stream);
+    nfs::dev_free(d_vox); nfs::dev_free(d_b0); nfs::dev_free(d_rr); nfs::dev_free(d_tt); nfs::dev_free(d_max);
+  };
+  cudaError_t e = nfs::dev_alloc((void**)&d_vox, std::max<size_t>(L * 8, 8));
+  if (e == cudaSuccess) e = nfs::dev_alloc((void**)&d_b0, std::max<size_t>(L * 8, 8));
+  if (e == cudaSuccess) e = nfs::dev_alloc((void**)&d_rr, std::max<size_t>((size_t)L * nt * 8, 8));
+  if (e == cudaSuccess) e = nfs::dev_alloc((void**)&d_max, nt * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_vox, vox_index, L * 8, cudaMemcpyHostToDevice, P->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_b0, b0_masked, L * 8, cudaMemcpyHostToDevice, P->stream);
+  if (e == cudaSuccess) e = nfs::launch_spatial_from_grid(d_vox, d_b0, L, nt, dims, fov, order, d_rr, P->stream);
+  if (e == cudaSuccess) {
+    if (P->esz == 8) {
+      e = cudaMemcpyAsync(P->d_T, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice, P->stream);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(P->d_R, d_rr, (size_t)L * nt * 8, cudaMemcpyDeviceToDevice, P->stream);
+    } else {
+      std::vector<float> tf(tt.begin(), tt.end());
+      e = cudaMemcpyAsync(P->d_T, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice, P->stream);
+      if (e == cudaSuccess) e = nfs::launch_to_float(d_rr, (float*)P->d_R, (int64_t)L * nt, P->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);   // tf goes out of scope
+    }
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) {
+    cleanup();
+    return fail(NFS_ERR_CUDA, std::string("device bases: ") + cudaGetErrorString(e));
+  }
+  P->have_tables = true;
+  if (P->tc) {
+    int st = nfs::tc_set_tables(P->tc, P->d_T, P->d_R, P->stream);
+    if (st) { cleanup(); return fail(NFS_ERR_CUDA, "tc tables: " + std::string(nfs::tc_last_error())); }
+  }
+  if (P->tci) {
+    std::vector<unsigned long long> mx(nt, 0ull);
+    e = nfs::launch_col_absmax(d_rr, L, nt, d_max, P->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(mx.data(), d_max, nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, P->stream);
+    if (e == cudaSuccess) e = nfs::dev_alloc((void**)&d_tt, std::max<size_t>(tt.size() * 8, 8));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_tt, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice, P->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
+    if (e != cudaSuccess) { cleanup(); return fail(NFS_ERR_CUDA, std::string("device bases: ") + cudaGetErrorString(e)); }
+    for (int p = 0; p < nt; ++p) {
+      long long bits = (long long)mx[p];
+      memcpy(&amax_r[p], &bits, 8);
+    }
+    int st = nfs::tci_set_tables_dev(P->tci, d_tt, d_rr, amax_t.data(), amax_r.data(), P->stream);
+    if (st == 2) {
+      nfs::tci_destroy(P->tci);
+      P->tci = nullptr;
+      P->desc += " [f16x3 unavailable for this basis (phase range): FP32 CUDA-core contraction]";
+    } else if (st) {
+      cleanup();
+      return fail(NFS_ERR_INVALID, "tci tables: " + std::string(nfs::tci_last_error()));
+    }
+  }
+  cleanup();
   return NFS_OK;
 }
 

@@ -15,6 +15,10 @@ const char* tci_describe(TciPlan* t);
 const char* tci_last_error();
 // tables on the host: temporal in turns [K][nt], spatial [L][nt] (FP64, zero padded)
 int tci_set_tables(TciPlan* t, const double* tt_turns, const double* rr, cudaStream_t st);
+// same from FP64 device tables [K][nt] / [L][nt] and their per-term max |value| (host arrays);
+// returns 2 when the exact fixed-point phase range is exceeded
+int tci_set_tables_dev(TciPlan* t, const double* d_tt, const double* d_rr, const double* amax_t,
+                       const double* amax_r, cudaStream_t st);
 int tci_set_sens(TciPlan* t, const void* d_S, int ldc, cudaStream_t st);
 // part 0 = prep + main kernel, part 1 = split reduction
 int tci_forward_parts(TciPlan* t, const double2* p, void* y, const int* stop, cudaStream_t st, int part);

@@ -109,6 +109,42 @@ class CGLog:
 # lazy phase handle (nfs/engine.py:93-95)
 # ----------------------------------------------------------------------------------
 
+class DeviceSpatial:
+    """Spatial basis (P+1, L_R) described by the grid, mask, B0 map and harmonic order; the
+    table is evaluated on the GPU by `nfs_set_tables_grid`, so only a voxel index
+    and B0 per voxel cross PCIe.  `np.asarray(handle)` builds the identical host table with the
+    reference formulas (nfs/engine.py:252-280), so it can stand in for the array anywhere.
+    """
+
+    __array_priority__ = 10
+
+    def __init__(self, b0, mask_r, grid: Grid, order: int):
+        self.mask_r = np.asarray(mask_r, dtype=bool).reshape(-1)
+        self.b0 = np.asarray(b0, dtype=float).reshape(-1)
+        if self.b0.size != self.mask_r.size or self.mask_r.size != grid.nvox:
+            raise EngineError("B0 map and mask must cover the grid")
+        if order not in (1, 2, 3):
+            raise EngineError(f"unsupported harmonic order {order}")
+        self.grid, self.order = grid, int(order)
+        self.vox_index = np.flatnonzero(self.mask_r).astype(np.int64)
+        self.b0_masked = np.ascontiguousarray(self.b0[self.mask_r])
+        n_h = {1: 2 if grid.ndim == 2 else 3, 2: 8, 3: 15}[self.order]
+        self.shape = (1 + n_h, int(self.vox_index.size))
+
+    @property
+    def dtype(self):
+        return np.dtype(np.float64)
+
+    def __array__(self, dtype=None, copy=None):
+        coords = grid_coordinates(self.grid)[self.mask_r]
+        harm = solid_harmonics(self.order, coords, ndim=self.grid.ndim)
+        arr = np.vstack([self.b0_masked[None, :], harm.T])
+        return arr if dtype is None else arr.astype(dtype)
+
+    def upload(self, plan, temporal):
+        plan.set_tables_grid(temporal, self.vox_index, self.b0_masked, self.grid.dims, self.grid.fov_m, self.order)
+
+
 class PhaseBlock:
     """P' = exp(i * temporal_rows @ spatial), never materialised on the hot path.
 
@@ -235,7 +271,10 @@ def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label:
     plan.set_sens(inputs.sens, inputs.intensity)          # S' = S o j on upload
     log.add_timing("intensity_correction", time.perf_counter() - t0)
     t0 = time.perf_counter()
-    plan.set_tables(inputs.temporal[lo:hi], inputs.spatial)
+    if isinstance(inputs.spatial, DeviceSpatial):
+        inputs.spatial.upload(plan, inputs.temporal[lo:hi])
+    else:
+        plan.set_tables(inputs.temporal[lo:hi], inputs.spatial)
     if timing_label:   # the GPU analogue of building P: plan + table upload
         log.add_timing("build_phase_matrix", t_plan + time.perf_counter() - t0)
     plan.set_samples(inputs.sigma[lo:hi])
@@ -316,19 +355,29 @@ def choose_block_starts(n_samples: int, n_voxels: int, memory_budget_bytes: int)
     return np.unique(np.asarray(list(range(0, n_samples, rows)) + [n_samples], dtype=int))
 
 
-def build_bases(b0, mask_r, grid: Grid, times_s, field_terms, order: int = 1):
-    """Spatial (P+1, L_R) and temporal (K, P+1) basis tables (nfs/engine.py:252-280)."""
+def build_bases(b0, mask_r, grid: Grid, times_s, field_terms, order: int = 1, *, on_device: bool = False):
+    """Spatial (P+1, L_R) and temporal (K, P+1) basis tables (nfs/engine.py:252-280).
+
+    `on_device=True` returns a `DeviceSpatial` handle instead of the spatial array: recon_full /
+    recon_split then evaluate the table on the GPU; `np.asarray(handle)` gives the
+    identical host array.
+    """
     mask_r = np.asarray(mask_r, dtype=bool).reshape(-1)
     b0 = np.asarray(b0, dtype=float).reshape(-1)
-    coords = grid_coordinates(grid)[mask_r]
-    harm = solid_harmonics(order, coords, ndim=grid.ndim)
+    if on_device:
+        spatial = DeviceSpatial(b0, mask_r, grid, order)   # table evaluated on the GPU at upload
+        n_h = spatial.shape[0] - 1
+    else:
+        harm = solid_harmonics(order, grid_coordinates(grid)[mask_r], ndim=grid.ndim)
+        spatial, n_h = None, harm.shape[1]
     field_terms = np.asarray(field_terms, dtype=float)
-    if field_terms.ndim != 2 or field_terms.shape[1] != harm.shape[1]:
+    if field_terms.ndim != 2 or field_terms.shape[1] != n_h:
         got = field_terms.shape[1] if field_terms.ndim == 2 else "?"
-        raise EngineError(f"trajectory provides {got} field terms but order {order} needs {harm.shape[1]}")
+        raise EngineError(f"trajectory provides {got} field terms but order {order} needs {n_h}")
     times_s = np.asarray(times_s, dtype=float).reshape(-1)
     if times_s.size != field_terms.shape[0]:
         raise EngineError("sample time count does not match field terms")
-    spatial = np.vstack([b0[mask_r][None, :], harm.T])
     temporal = np.column_stack([times_s, field_terms])
+    if spatial is None:
+        spatial = np.vstack([b0[mask_r][None, :], harm.T])
     return spatial, temporal

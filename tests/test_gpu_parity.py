@@ -334,3 +334,54 @@ def test_f16x3_phase_range_fallback():
             assert "FP32 CUDA-core contraction" in plan.describe()
         plan.close()
     assert rel(out["f16x3"], out["fp32"]) < 1e-5
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32", "f16x3", "tf32x3"])
+def test_device_bases_bitwise(prec):
+    """the spatial table evaluated on the GPU (nfs_set_tables_grid) is bit-identical
+    to the host build_bases table, so every operator result is bit-identical too."""
+    rng = np.random.default_rng(4)
+    for dims, order, coils in (((24, 20, 1), 3, 8), ((10, 8, 6), 2, 4)):
+        grid = Grid(dims, (0.22, 0.2, 0.12))
+        mask = rng.random(grid.nvox) < 0.7
+        b0 = rng.standard_normal(grid.nvox) * 80.0
+        n_h = {1: 2 if grid.ndim == 2 else 3, 2: 8, 3: 15}[order]
+        K = 700
+        times = np.linspace(0.0, 0.02, K)
+        terms = rng.standard_normal((K, n_h)) * 30.0
+        s_host, temporal = engine.build_bases(b0, mask, grid, times, terms, order)
+        s_dev, _ = engine.build_bases(b0, mask, grid, times, terms, order, on_device=True)
+        L = s_host.shape[1]
+        sens = rng.standard_normal((L, coils)) + 1j * rng.standard_normal((L, coils))
+        p = rng.standard_normal(L) + 1j * rng.standard_normal(L)
+        outs = []
+        for use_dev in (False, True):
+            plan = Plan(K, L, coils, 1 + n_h, prec)
+            if use_dev:
+                s_dev.upload(plan, temporal)
+            else:
+                plan.set_tables(temporal, s_host)
+            plan.set_sens(sens)
+            outs.append((plan.apply_E(p), plan.apply_EHE(p)))
+            plan.close()
+        assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_recon_with_device_bases_matches_host_bases():
+    """recon_full with build_bases(on_device=True) equals recon_full with the host table."""
+    g = golden("engine8")
+    grid = Grid((8, 8, 1), (0.08, 0.08, 0.002))
+    rng = np.random.default_rng(8)
+    b0 = rng.standard_normal(grid.nvox) * 40.0
+    mask = np.ones(grid.nvox, bool)
+    K = g["sigma"].shape[0]
+    times = np.linspace(0.0, 0.01, K)
+    terms = rng.standard_normal((K, 2)) * 20.0
+    imgs = []
+    for on_dev in (False, True):
+        spatial, temporal = engine.build_bases(b0, mask, grid, times, terms, 1, on_device=on_dev)
+        sens = g["sens"]
+        inputs = inputs_from(grid, g["sigma"], spatial, temporal, sens, 8)
+        img, _ = engine.recon_full(inputs, precision="fp64")
+        imgs.append(img.values)
+    assert np.array_equal(imgs[0], imgs[1])

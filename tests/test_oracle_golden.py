@@ -127,3 +127,22 @@ def test_config_b_generators_and_rows():
 def test_block_starts(n, v, b):
     s = orc.choose_block_starts(n, v, b)
     assert s[0] == 0 and s[-1] == n and np.all(np.diff(s) > 0)
+
+
+def test_device_spatial_handle_matches_host_bases():
+    """build_bases(on_device=True) describes the same table the host builds."""
+    from paper_2604_09233_b200 import engine
+    from paper_2604_09233_b200.core import Grid
+    rng = np.random.default_rng(3)
+    for dims, order in (((12, 10, 1), 1), ((12, 10, 1), 3), ((6, 5, 4), 2), ((6, 5, 4), 3)):
+        grid = Grid(dims, (0.2, 0.18, 0.1))
+        mask = rng.random(grid.nvox) < 0.6
+        b0 = rng.standard_normal(grid.nvox) * 50
+        n_h = {1: 2 if grid.ndim == 2 else 3, 2: 8, 3: 15}[order]
+        t = np.linspace(0, 0.01, 7)
+        terms = rng.standard_normal((7, n_h))
+        s_host, t_host = engine.build_bases(b0, mask, grid, t, terms, order)
+        s_dev, t_dev = engine.build_bases(b0, mask, grid, t, terms, order, on_device=True)
+        assert isinstance(s_dev, engine.DeviceSpatial) and s_dev.shape == s_host.shape
+        assert np.array_equal(np.asarray(s_dev), s_host) and np.array_equal(t_dev, t_host)
+        assert np.array_equal(s_dev.vox_index, np.flatnonzero(mask))
