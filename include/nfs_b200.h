@@ -78,6 +78,16 @@ int nfs_set_sens(nfs_plan* plan, const double* sens, const double* intensity);
 /* Raw samples of this rank (K x G complex); non-finite -> NFS_ERR_NONFINITE. */
 int nfs_set_samples(nfs_plan* plan, const double* sigma);
 
+/* Per-iteration diagnostic on the device: relative RMSE of the image rho o j vs
+ * a reference (nfs/metrics.py:73-88 as called from a convergence-study callback) is logged by
+ * nfs_cg_solve without copying the iterate to the host.  ref_masked: reference on the
+ * reconstruction mask (L_R complex, zero off the RMSE support); weight: j on the support, 0 off;
+ * outside_sq: the support's |ref|^2 outside the mask; ref_sq: the support's |ref|^2.
+ * ref_masked == NULL turns it off.  nfs_rmse_log copies the first n logged values. */
+int nfs_set_rmse_reference(nfs_plan* plan, const double* ref_masked, const double* weight,
+                           double outside_sq, double ref_sq);
+int nfs_rmse_log(nfs_plan* plan, double* out, int32_t n);
+
 /* Operators with host buffers (copies inside).  nfs/engine.py:98-108. */
 int nfs_apply_E(nfs_plan* plan, const double* p, double* y);
 int nfs_apply_EH(nfs_plan* plan, const double* sigma, double* q);

@@ -8,6 +8,7 @@ and signatures, backed by hand-written sm_100a CUDA kernels behind a C ABI
 from .core import Grid, ReconImage, grid_coordinates
 from .engine import (
     CGLog,
+    DeviceRMSE,
     DeviceSpatial,
     EncodingInputs,
     EngineError,
@@ -22,7 +23,7 @@ from .engine import (
 )
 
 __all__ = [
-    "CGLog", "DeviceSpatial", "EncodingInputs", "EngineError", "Grid", "MemoryBudgetError", "ReconImage",
+    "CGLog", "DeviceRMSE", "DeviceSpatial", "EncodingInputs", "EngineError", "Grid", "MemoryBudgetError", "ReconImage",
     "apply_E", "apply_EH", "build_bases", "choose_block_starts", "grid_coordinates",
     "phase_block", "recon_full", "recon_split",
 ]

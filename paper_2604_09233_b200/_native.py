@@ -48,6 +48,8 @@ SIGNATURES = {
     "nfs_cg_solve": (_c_i32, [_c_void_p, _c_i32, CALLBACK, _c_void_p, _c_dbl_p, _c_dbl_p, _c_dbl_p,
                               ctypes.POINTER(_c_i32), _c_dbl_p]),
     "nfs_apply_EHE_resident": (_c_i32, [_c_void_p, _c_i32]),
+    "nfs_set_rmse_reference": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p, ctypes.c_double, ctypes.c_double]),
+    "nfs_rmse_log": (_c_i32, [_c_void_p, _c_dbl_p, _c_i32]),
     "nfs_kernel_times": (_c_i32, [_c_void_p, _c_i32, ctypes.POINTER(ctypes.c_float)]),
     "nfs_launches_per_apply": (_c_i32, [_c_void_p]),
     "nfs_plan_describe": (ctypes.c_char_p, [_c_void_p]),
@@ -220,6 +222,22 @@ class Plan:
         _check(status)
         n = int(done.value)
         return rho, res[:n].tolist(), sol[:n].tolist(), tim, n
+
+    def set_rmse_reference(self, ref_masked, weight, outside_sq, ref_sq):
+        """Device per-iteration RMSE diagnostic; None switches it off."""
+        _, l, _, _ = self.shape
+        if ref_masked is None:
+            _check(self._lib.nfs_set_rmse_reference(self._h, None, None, 0.0, 0.0))
+            return
+        r = _c128(ref_masked, (l,))
+        w = np.ascontiguousarray(weight, dtype=np.float64).reshape(l)
+        _check(self._lib.nfs_set_rmse_reference(self._h, _dp(r.view(np.float64)), _dp(w),
+                                                float(outside_sq), float(ref_sq)))
+
+    def rmse_log(self, n: int):
+        out = np.zeros(max(int(n), 1))
+        _check(self._lib.nfs_rmse_log(self._h, _dp(out), int(n)))
+        return out[:int(n)].tolist()
 
     # -- benchmarking ------------------------------------------------------------------
     def apply_EHE_resident(self, n: int):

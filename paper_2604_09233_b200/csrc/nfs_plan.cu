@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <string>
 #include <vector>
 
@@ -108,6 +109,13 @@ struct nfs_plan {
   nfs::TcPlan* tc = nullptr;            // tensor-core operator, FP32 phase (NFS_PREC_TF32X3)
   nfs::TciPlan* tci = nullptr;          // tensor-core operator, exact int8 phase (NFS_PREC_F16X3)
   std::string desc;
+  // device RMSE diagnostic (nfs_set_rmse_reference)
+  double2* d_rmse_ref = nullptr;
+  double* d_rmse_w = nullptr;
+  double* d_rmse_log = nullptr;
+  double rmse_outside = 0.0, rmse_ref_sq = 0.0;
+  int rmse_cap = 0;
+  bool rmse_on = false;
 };
 
 static size_t t2size(const nfs_plan* P) { return 2 * P->esz; }
@@ -265,7 +273,7 @@ extern "C" void nfs_plan_destroy(nfs_plan* P) {
   if (P->tci) nfs::tci_destroy(P->tci);
   void* bufs[] = {P->d_T, P->d_R, P->d_S, P->d_sig, P->d_y, P->d_w, P->d_party, P->d_partq,
                   P->d_p, P->d_q, P->d_r, P->d_rho, P->d_q0, P->d_io, P->d_partials,
-                  P->d_cg, P->d_res, P->d_sol};
+                  P->d_cg, P->d_res, P->d_sol, P->d_rmse_ref, P->d_rmse_w, P->d_rmse_log};
   for (void* b : bufs)
     if (b) nfs::dev_free(b);
   if (P->comm && nccl_api().ok) nccl_api().destroy(P->comm);
@@ -618,6 +626,45 @@ static int cg_iteration(nfs_plan* P) {
   NFS_TRY(run_ehe(P, P->d_p, P->d_q, stop));
   NFS_CUDA(nfs::launch_cg_iter_tail(P->d_q, P->d_p, P->d_r, P->d_rho, P->L, P->d_cg,
                                     P->d_partials, P->d_res, P->d_sol, P->stream));
+  if (P->rmse_on)
+    NFS_CUDA(nfs::launch_cg_rmse(P->d_rho, P->d_rmse_ref, P->d_rmse_w, P->L, P->d_cg, P->d_partials,
+                                 P->rmse_outside, P->rmse_ref_sq, P->d_rmse_log, P->stream));
+  return NFS_OK;
+}
+
+// Device-side per-iteration relative RMSE of rho o j vs a reference image: no
+// host copy of the iterate per iteration.  ref_masked: reference on the reconstruction mask
+// (L_R complex, zero off the RMSE support); weight: j on the support, 0 off it; outside_sq: the
+// support's |ref|^2 outside the reconstruction mask; ref_sq: the support's total |ref|^2.
+// ref_masked == NULL switches the diagnostic off.
+extern "C" int nfs_set_rmse_reference(nfs_plan* P, const double* ref_masked, const double* weight,
+                                      double outside_sq, double ref_sq) {
+  if (!P) return fail(NFS_ERR_INVALID, "null plan");
+  if (!ref_masked) {
+    P->rmse_on = false;
+    return NFS_OK;
+  }
+  if (!weight || !(ref_sq > 0.0) || !std::isfinite(ref_sq) || !(outside_sq >= 0.0))
+    return fail(NFS_ERR_INVALID, "RMSE reference is zero on the support");
+  NFS_CUDA(cudaSetDevice(P->device));
+  if (!P->d_rmse_ref) {
+    NFS_CUDA(nfs::dev_alloc((void**)&P->d_rmse_ref, std::max<int64_t>(P->L, 1) * sizeof(double2)));
+    NFS_CUDA(nfs::dev_alloc((void**)&P->d_rmse_w, std::max<int64_t>(P->L, 1) * sizeof(double)));
+  }
+  NFS_CUDA(cudaMemcpyAsync(P->d_rmse_ref, ref_masked, P->L * sizeof(double2), cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(cudaMemcpyAsync(P->d_rmse_w, weight, P->L * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
+  P->rmse_outside = outside_sq;
+  P->rmse_ref_sq = ref_sq;
+  P->rmse_on = true;
+  return NFS_OK;
+}
+
+// per-iteration RMSE values of the last nfs_cg_solve (n <= iterations done)
+extern "C" int nfs_rmse_log(nfs_plan* P, double* out, int32_t n) {
+  if (!P || !out || n < 0) return fail(NFS_ERR_INVALID, "bad arguments");
+  if (!P->rmse_on || n > P->rmse_cap) return fail(NFS_ERR_INVALID, "no RMSE log of that length");
+  if (n > 0) NFS_CUDA(cudaMemcpy(out, P->d_rmse_log, n * sizeof(double), cudaMemcpyDeviceToHost));
   return NFS_OK;
 }
 
@@ -636,6 +683,13 @@ extern "C" int nfs_cg_solve(nfs_plan* P, int32_t n_iter, nfs_iter_callback cb, v
     NFS_CUDA(nfs::dev_alloc((void**)&P->d_res, std::max(n_iter, 1) * sizeof(double)));
     NFS_CUDA(nfs::dev_alloc((void**)&P->d_sol, std::max(n_iter, 1) * sizeof(double)));
     P->log_cap = n_iter;
+  }
+  if (P->rmse_on && n_iter > P->rmse_cap) {
+    cudaStreamSynchronize(P->stream);
+    nfs::dev_free(P->d_rmse_log);
+    P->d_rmse_log = nullptr;
+    NFS_CUDA(nfs::dev_alloc((void**)&P->d_rmse_log, std::max(n_iter, 1) * sizeof(double)));
+    P->rmse_cap = n_iter;
   }
   std::vector<cudaEvent_t> ev(n_iter + 2);
   for (auto& e : ev) NFS_CUDA(cudaEventCreate(&e));

@@ -242,6 +242,30 @@ __global__ void cg_dir_kernel(const double2* __restrict__ r, double2* __restrict
   }
 }
 
+// per-iteration relative RMSE of the image rho o j against a reference, on the device (SURVEY 8f
+// f4; the reference's metrics.rmse, nfs/metrics.py:73-88, evaluated in a convergence study's
+// callback): err^2 = (sum_l w_l^2-weighted |rho_l w_l - ref_l|^2 + outside) / ref_sq, where
+// w_l = j_l on the RMSE support and 0 off it (then ref_l = 0 too), and `outside` is the
+// support's energy outside the reconstruction mask (the image is zero there).
+__global__ void cg_rmse_kernel(const double2* __restrict__ rho, const double2* __restrict__ ref,
+                               const double* __restrict__ w, int64_t n, CGState* st, double* partials,
+                               double outside, double ref_sq, double* log) {
+  if (st->err || st->iter < 1) return;
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 x = rho[i], r = ref[i];
+    const double dx = x.x * w[i] - r.x, dy = x.y * w[i] - r.y;
+    v[0] = fma(dx, dx, fma(dy, dy, v[0]));
+  }
+  double tot[1];
+  if (grid_sum<1>(v, partials, &st->ticket, tot) && threadIdx.x == 0)
+    log[st->iter - 1] = sqrt((tot[0] + outside) / ref_sq);
+}
+
+cudaError_t launch_cg_rmse(const double2* rho, const double2* ref, const double* w, int64_t n, CGState* s,
+                           double* partials, double outside, double ref_sq, double* log, cudaStream_t st);
+
 // ------------------------------------------------------------------ phase materialisation
 template <typename T, int NT>
 __global__ void phase_rows_kernel(const T* __restrict__ ttab, const T* __restrict__ rtab,
@@ -316,6 +340,12 @@ cudaError_t launch_cg_iter_tail(const double2* q, double2* p, double2* r, double
   cg_dot_kernel<<<gb, 256, 0, st>>>(p, q, n, s, partials);
   cg_update_kernel<<<gb, 256, 0, st>>>(p, q, r, rho, n, s, partials, res_log, sol_log);
   cg_dir_kernel<<<gb, 256, 0, st>>>(r, p, n, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_rmse(const double2* rho, const double2* ref, const double* w, int64_t n, CGState* s,
+                           double* partials, double outside, double ref_sq, double* log, cudaStream_t st) {
+  cg_rmse_kernel<<<cg_grid(n), 256, 0, st>>>(rho, ref, w, n, s, partials, outside, ref_sq, log);
   return cudaGetLastError();
 }
 

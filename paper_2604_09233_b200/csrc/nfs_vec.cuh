@@ -26,6 +26,8 @@ cudaError_t launch_reduce_parts(int prec, const void* part, void* out, int64_t n
 cudaError_t launch_reduce_image(int prec, const void* part, double2* q, int64_t n, int n_part,
                                 const int* stop, cudaStream_t st);
 int cg_grid(int64_t n);
+cudaError_t launch_cg_rmse(const double2* rho, const double2* ref, const double* w, int64_t n, CGState* s,
+                           double* partials, double outside, double ref_sq, double* log, cudaStream_t st);
 cudaError_t launch_cg_init(const double2* q0, double2* r, double2* p, double2* rho, int64_t n,
                            CGState* s, double* partials, cudaStream_t st);
 cudaError_t launch_cg_iter_tail(const double2* q, double2* p, double2* r, double2* rho, int64_t n,

@@ -145,6 +145,41 @@ class DeviceSpatial:
         plan.set_tables_grid(temporal, self.vox_index, self.b0_masked, self.grid.dims, self.grid.fov_m, self.order)
 
 
+class DeviceRMSE:
+    """Convergence-study callback computed on the GPU.
+
+    Equivalent to the reference pattern (tests/test_acceptance.py:346-375)::
+
+        def cb(n, rho_r):
+            full = zeros(L); full[mask_r] = rho_r * j; errs.append(metrics.rmse(full, ref, support))
+
+    Passed as `callback=` to recon_full / recon_split, the relative RMSE of every iterate is
+    evaluated inside the device CG loop (no per-iteration host copy of the iterate) and lands in
+    `.values` when the solve returns (one value per completed iteration).
+    """
+
+    def __init__(self, reference, support=None):
+        self.reference = np.asarray(reference).reshape(-1)
+        self.support = None if support is None else np.asarray(support, dtype=bool).reshape(-1)
+        self.values: list = []
+
+    def _restricted(self, mask_r, intensity):
+        sup = np.ones(self.reference.size, bool) if self.support is None else self.support
+        if sup.size != mask_r.size or self.reference.size != mask_r.size:
+            raise EngineError("RMSE reference / support must cover the grid")
+        ref_sq = float(np.sum(np.abs(self.reference[sup]) ** 2))
+        if ref_sq == 0.0:
+            raise EngineError("reference is zero on the mask")
+        on = sup[mask_r]
+        ref_m = np.where(on, self.reference[mask_r], 0.0).astype(np.complex128)
+        w = np.where(on, np.asarray(intensity, dtype=float), 0.0)
+        outside = float(np.sum(np.abs(self.reference[sup & ~mask_r]) ** 2))
+        return ref_m, w, outside, ref_sq
+
+    def __call__(self, n, rho_r):
+        raise EngineError("DeviceRMSE is evaluated on the device by recon_full / recon_split")
+
+
 class PhaseBlock:
     """P' = exp(i * temporal_rows @ spatial), never materialised on the hot path.
 
@@ -282,13 +317,19 @@ def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label:
 
 
 def _run_cg(plan, inputs: EncodingInputs, log: CGLog, callback):
+    device_rmse = isinstance(callback, DeviceRMSE)
+    if device_rmse:
+        plan.set_rmse_reference(*callback._restricted(inputs.mask_r, inputs.intensity))
+        callback = None
     rho, res, sol, tim, n_done = plan.cg_solve(inputs.n_iter, callback)
+    if device_rmse:
+        device_rmse = plan.rmse_log(n_done)
     log.add_timing("initial_adjoint", float(tim[0]))
     for n in range(1, n_done + 1):
         log.add_timing(f"cg_iteration_{n}", float(tim[1 + n]))
     log.residual_norms.extend(res)
     log.solution_norms.extend(sol)
-    return rho
+    return rho, device_rmse
 
 
 def _finalize(rho_r: np.ndarray, inputs: EncodingInputs, log: CGLog) -> ReconImage:
@@ -324,7 +365,9 @@ def recon_full(inputs: EncodingInputs, memory_budget_bytes: int | None = None, c
         raise EngineError("raw data contains non-finite values")
     plan = _make_plan(inputs, precision or default_precision(), log, timing_label=True)
     try:
-        rho = _run_cg(plan, inputs, log, callback)
+        rho, rmse_values = _run_cg(plan, inputs, log, callback)
+        if isinstance(callback, DeviceRMSE):
+            callback.values = rmse_values
     finally:
         plan.close()
     return _finalize(rho, inputs, log), log
@@ -343,7 +386,9 @@ def recon_split(inputs: EncodingInputs, callback=None, *, precision: str | None 
         raise EngineError("raw data contains non-finite values")
     plan = _make_plan(inputs, precision or default_precision(), log, timing_label=False)
     try:
-        rho = _run_cg(plan, inputs, log, callback)
+        rho, rmse_values = _run_cg(plan, inputs, log, callback)
+        if isinstance(callback, DeviceRMSE):
+            callback.values = rmse_values
     finally:
         plan.close()
     return _finalize(rho, inputs, log), log

@@ -385,3 +385,37 @@ def test_recon_with_device_bases_matches_host_bases():
         img, _ = engine.recon_full(inputs, precision="fp64")
         imgs.append(img.values)
     assert np.array_equal(imgs[0], imgs[1])
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-12), ("f16x3", 1e-12)])
+def test_device_rmse_diagnostic(prec, tol):
+    """DeviceRMSE logs the per-iteration relative RMSE inside the device CG loop and
+    equals the reference's callback pattern (tests/test_acceptance.py:346-375) evaluated on the
+    host on the same iterates."""
+    rng = np.random.default_rng(21)
+    grid = Grid((16, 16, 1), (0.16, 0.16, 0.002))
+    mask = rng.random(grid.nvox) < 0.7
+    support = rng.random(grid.nvox) < 0.6          # partly outside the reconstruction mask
+    L = int(mask.sum())
+    K, G = 400, 4
+    spatial = rng.standard_normal((3, L)) * 0.5
+    temporal = rng.standard_normal((K, 3)) * 3.0
+    sens = rng.standard_normal((L, G)) + 1j * rng.standard_normal((L, G))
+    j = 0.5 + rng.random(L)
+    sigma = rng.standard_normal((K, G)) + 1j * rng.standard_normal((K, G))
+    ref = rng.standard_normal(grid.nvox) + 1j * rng.standard_normal(grid.nvox)
+
+    def host_rmse(rho_r):
+        full = np.zeros(grid.nvox, complex)
+        full[mask] = rho_r * j
+        t, r = full[support], ref[support]
+        return np.sqrt(np.mean(np.abs(t - r) ** 2)) / np.sqrt(np.mean(np.abs(r) ** 2))
+
+    host = []
+    inp = inputs_from(grid, sigma, spatial, temporal, sens, 12, mask=mask, intensity=j)
+    engine.recon_full(inp, callback=lambda n, r: host.append(host_rmse(r)), precision=prec)
+    dev = engine.DeviceRMSE(ref, support)
+    inp = inputs_from(grid, sigma, spatial, temporal, sens, 12, mask=mask, intensity=j)
+    engine.recon_full(inp, callback=dev, precision=prec)
+    assert len(dev.values) == len(host) == 12
+    assert np.max(np.abs(np.array(dev.values) - np.array(host)) / np.array(host)) < tol
