@@ -146,3 +146,26 @@ def test_device_spatial_handle_matches_host_bases():
         assert isinstance(s_dev, engine.DeviceSpatial) and s_dev.shape == s_host.shape
         assert np.array_equal(np.asarray(s_dev), s_host) and np.array_equal(t_dev, t_host)
         assert np.array_equal(s_dev.vox_index, np.flatnonzero(mask))
+
+
+def test_device_rmse_restriction_host_logic():
+    """DeviceRMSE's restriction (reference on the mask, weights, outside energy) reproduces the
+    reference callback's metrics.rmse for any iterate (host-side check of the device inputs)."""
+    from paper_2604_09233_b200 import engine
+    rng = np.random.default_rng(9)
+    n = 300
+    mask = rng.random(n) < 0.6
+    support = rng.random(n) < 0.5
+    ref = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    j = 0.5 + rng.random(int(mask.sum()))
+    rho = rng.standard_normal(int(mask.sum())) + 1j * rng.standard_normal(int(mask.sum()))
+    ref_m, w, outside, ref_sq = engine.DeviceRMSE(ref, support)._restricted(mask, j)
+    dev = np.sqrt((np.sum(np.abs(rho * w - ref_m) ** 2) + outside) / ref_sq)
+    full = np.zeros(n, complex)
+    full[mask] = rho * j
+    host = np.sqrt(np.mean(np.abs(full[support] - ref[support]) ** 2)) / np.sqrt(np.mean(np.abs(ref[support]) ** 2))
+    assert abs(dev - host) / host < 1e-12
+    with pytest.raises(engine.EngineError):
+        engine.DeviceRMSE(np.zeros(n), support)._restricted(mask, j)
+    with pytest.raises(engine.EngineError):
+        engine.DeviceRMSE(ref, support)(1, rho)
