@@ -21,7 +21,7 @@ __device__ __forceinline__ void f16_split2(float x, float y, uint32_t& hi, uint3
 }
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 template <int NI, int MODE>
-__global__ void k(int iters, uint32_t* out, long long* cyc) {
+__global__ void __launch_bounds__(512, 1) k(int iters, uint32_t* out, long long* cyc) {
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
   if (MODE >= 2) {
@@ -44,10 +44,15 @@ __global__ void k(int iters, uint32_t* out, long long* cyc) {
         f16_split2(c0, s0, hl[i], hl[8 + i]);
         f16_split2(c1, s1, hl[i + 1], hl[8 + i + 1]);
       }
-      if (MODE >= 2) {
+      if (MODE >= 2 && MODE != 6) {
         asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" :: "r"(tb + 384 + ((warp >> 2) & 1) * 64 + (sl / 8 % 4) * 16),
           "r"(hl[0]),"r"(hl[1]),"r"(hl[2]),"r"(hl[3]),"r"(hl[4]),"r"(hl[5]),"r"(hl[6]),"r"(hl[7]),"r"(hl[8]),"r"(hl[9]),"r"(hl[10]),"r"(hl[11]),"r"(hl[12]),"r"(hl[13]),"r"(hl[14]),"r"(hl[15]) : "memory");
-        if (MODE == 4) {   // pipelined: wait for the load issued one slice earlier, then issue the next
+      }
+      if (MODE == 6) {
+        for (int i = 0; i < 16; ++i) acc += hl[i];
+      }
+      if (MODE >= 2) {
+        if (MODE == 4 || MODE == 6) {   // pipelined: wait for the load issued one slice earlier, then issue the next
           if (sl > 0) {
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
@@ -56,6 +61,25 @@ __global__ void k(int iters, uint32_t* out, long long* cyc) {
           asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
             : "=r"(pv[0]),"=r"(pv[1]),"=r"(pv[2]),"=r"(pv[3]),"=r"(pv[4]),"=r"(pv[5]),"=r"(pv[6]),"=r"(pv[7]),"=r"(pv[8]),"=r"(pv[9]),"=r"(pv[10]),"=r"(pv[11]),"=r"(pv[12]),"=r"(pv[13]),"=r"(pv[14]),"=r"(pv[15]),"=r"(pv[16]),"=r"(pv[17]),"=r"(pv[18]),"=r"(pv[19]),"=r"(pv[20]),"=r"(pv[21]),"=r"(pv[22]),"=r"(pv[23]),"=r"(pv[24]),"=r"(pv[25]),"=r"(pv[26]),"=r"(pv[27]),"=r"(pv[28]),"=r"(pv[29]),"=r"(pv[30]),"=r"(pv[31])
             : "r"(tb + 128 + ((warp >> 2) & 1) * 128 + (sl / 8 % 4) * 32) : "memory");
+        }
+        if (MODE == 7 || MODE == 8) {
+          if (sl > 0) {
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < (MODE == 7 ? 8 : 4); ++i) t[sl - 8 + i] += pv[4 * i] + (pv[4 * i + 1] << 8) + (pv[4 * i + 2] << 16) + (pv[4 * i + 3] << 24);
+          }
+          if (MODE == 7) {
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(pv[0]),"=r"(pv[1]),"=r"(pv[2]),"=r"(pv[3]),"=r"(pv[4]),"=r"(pv[5]),"=r"(pv[6]),"=r"(pv[7]),"=r"(pv[8]),"=r"(pv[9]),"=r"(pv[10]),"=r"(pv[11]),"=r"(pv[12]),"=r"(pv[13]),"=r"(pv[14]),"=r"(pv[15])
+              : "r"(tb + 128 + ((warp >> 2) & 1) * 128 + (sl / 8 % 4) * 32) : "memory");
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(pv[16]),"=r"(pv[17]),"=r"(pv[18]),"=r"(pv[19]),"=r"(pv[20]),"=r"(pv[21]),"=r"(pv[22]),"=r"(pv[23]),"=r"(pv[24]),"=r"(pv[25]),"=r"(pv[26]),"=r"(pv[27]),"=r"(pv[28]),"=r"(pv[29]),"=r"(pv[30]),"=r"(pv[31])
+              : "r"(tb + 128 + ((warp >> 2) & 1) * 128 + (sl / 8 % 4) * 32 + 16) : "memory");
+          } else {
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(pv[0]),"=r"(pv[1]),"=r"(pv[2]),"=r"(pv[3]),"=r"(pv[4]),"=r"(pv[5]),"=r"(pv[6]),"=r"(pv[7]),"=r"(pv[8]),"=r"(pv[9]),"=r"(pv[10]),"=r"(pv[11]),"=r"(pv[12]),"=r"(pv[13]),"=r"(pv[14]),"=r"(pv[15])
+              : "r"(tb + 128 + ((warp >> 2) & 1) * 128 + (sl / 8 % 4) * 32) : "memory");
+          }
         }
         if (MODE == 3) {
           uint32_t v[32];
@@ -71,7 +95,7 @@ __global__ void k(int iters, uint32_t* out, long long* cyc) {
       for (int i = 0; i < 16; ++i) acc += hl[i];
       }
     }
-    if (MODE == 4) {
+    if (MODE == 4 || MODE == 6 || MODE == 7 || MODE == 8) {
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int i = 0; i < 8; ++i) t[NI - 8 + i] += pv[4 * i] + (pv[4 * i + 1] << 8) + (pv[4 * i + 2] << 16) + (pv[4 * i + 3] << 24);
@@ -103,7 +127,7 @@ __global__ void k(int iters, uint32_t* out, long long* cyc) {
 }
 int main() {
   uint32_t* o; long long* c; cudaMalloc(&o, 148 * 2048 * 4); cudaMallocManaged(&c, 8);
-  for (int mode = 2; mode < 5; ++mode)
+  for (int mode = 2; mode < 9; ++mode)
   for (int w = 4; w <= 16; w *= 2) {
     const int iters = 500;
     if (mode == 0) k<32, 0><<<148, w * 32>>>(iters, o, c);
@@ -111,8 +135,12 @@ int main() {
     if (mode == 2) k<32, 2><<<148, w * 32>>>(iters, o, c);
     if (mode == 3) k<32, 3><<<148, w * 32>>>(iters, o, c);
     if (mode == 4) k<32, 4><<<148, w * 32>>>(iters, o, c);
+    if (mode == 5) k<16, 4><<<148, w * 32>>>(iters, o, c);
+    if (mode == 6) k<32, 6><<<148, w * 32>>>(iters, o, c);
+    if (mode == 7) k<32, 7><<<148, w * 32>>>(iters, o, c);
+    if (mode == 8) k<32, 8><<<148, w * 32>>>(iters, o, c);
     cudaDeviceSynchronize();
-    const double mufu = (double)iters * 32 * 2 * w * 32;
+    const double mufu = (double)iters * (mode == 5 ? 16 : 32) * 2 * w * 32;
     printf("mode %d warps/SM=%2d: %.2f MUFU lane-ops/clk/SM (peak 16) -> %.0f%%\n", mode, w, mufu / *c, 100 * mufu / *c / 16);
   }
 }
