@@ -1,4 +1,5 @@
-// nfs_bases.cu -- spatial basis table evaluated on the device from voxel indices.
+// nfs_bases.cu -- device-side input preparation: basis tables (incl. the spatial basis evaluated
+// from voxel indices), S' = S o j, and the raw-data finiteness check.
 //
 // R[l, 0] = B0 (rad/s) of masked voxel l, R[l, 1..] = the zero-Laplacian solid harmonics of its
 // grid coordinates (order 1 / 2 / 3: 2-or-3 / 8 / 15 terms), in the plan's [L_R][NT] FP64 table
@@ -70,6 +71,55 @@ __global__ void to_float_kernel(const double* __restrict__ in, float* __restrict
     out[i] = (float)in[i];
 }
 
+// temporal [K][P1] (rad) -> tt [K][nt] (turns, zero padded); spatial [P1][L] -> rr [L][nt]
+__global__ void prep_tables_kernel(const double* __restrict__ temporal, const double* __restrict__ spatial,
+                                   int64_t K, int64_t L, int p1, int nt, double* __restrict__ tt,
+                                   double* __restrict__ rr) {
+  const double inv2pi = 1.0 / 6.283185307179586476925286766559;
+  const int64_t nk = K * nt, total = nk + L * nt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < nk) {
+      const int64_t k = i / nt;
+      const int p = (int)(i - k * nt);
+      tt[i] = p < p1 ? temporal[k * p1 + p] * inv2pi : 0.0;
+    } else {
+      const int64_t j = i - nk, l = j / nt;
+      const int p = (int)(j - l * nt);
+      rr[j] = p < p1 ? spatial[(int64_t)p * L + l] : 0.0;
+    }
+  }
+}
+
+// S' = S o j with the coil stride padded to ldc (FP32 or FP64 layout)
+template <typename T2>
+__global__ void prep_sens_kernel(const double2* __restrict__ sens, const double* __restrict__ j, int64_t L, int g,
+                                 int ldc, T2* __restrict__ out) {
+  const int64_t n = L * ldc;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = i / ldc;
+    const int c = (int)(i - l * ldc);
+    T2 v;
+    v.x = 0; v.y = 0;
+    if (c < g) {
+      const double w = j ? j[l] : 1.0;
+      const double2 s = sens[l * g + c];
+      v.x = s.x * w;
+      v.y = s.y * w;
+    }
+    out[i] = v;
+  }
+}
+
+// count of non-finite doubles (raw data check of nfs_set_samples)
+__global__ void count_nonfinite_kernel(const double* __restrict__ x, int64_t n, unsigned int* out) {
+  unsigned int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad += isfinite(x[i]) ? 0u : 1u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(out, bad);
+}
+
 int harmonic_terms(int order, int ndim) {
   if (order == 1) return ndim == 2 ? 2 : 3;
   if (order == 2) return 8;
@@ -95,6 +145,25 @@ cudaError_t launch_col_absmax(const double* d_tab, int64_t n, int nt, unsigned l
 
 cudaError_t launch_to_float(const double* d_in, float* d_out, int64_t n, cudaStream_t st) {
   to_float_kernel<<<grid_for(n), 256, 0, st>>>(d_in, d_out, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep_tables(const double* d_temporal, const double* d_spatial, int64_t K, int64_t L, int p1,
+                               int nt, double* d_tt, double* d_rr, cudaStream_t st) {
+  prep_tables_kernel<<<grid_for((K + L) * nt), 256, 0, st>>>(d_temporal, d_spatial, K, L, p1, nt, d_tt, d_rr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep_sens(const double2* d_sens, const double* d_j, int64_t L, int g, int ldc, bool fp64,
+                             void* d_out, cudaStream_t st) {
+  if (fp64) prep_sens_kernel<double2><<<grid_for(L * ldc), 256, 0, st>>>(d_sens, d_j, L, g, ldc, (double2*)d_out);
+  else prep_sens_kernel<float2><<<grid_for(L * ldc), 256, 0, st>>>(d_sens, d_j, L, g, ldc, (float2*)d_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_nonfinite(const double* d_x, int64_t n, unsigned int* d_out, cudaStream_t st) {
+  cudaMemsetAsync(d_out, 0, sizeof(unsigned int), st);
+  count_nonfinite_kernel<<<grid_for(n), 256, 0, st>>>(d_x, n, d_out);
   return cudaGetLastError();
 }
 

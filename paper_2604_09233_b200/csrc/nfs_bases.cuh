@@ -1,4 +1,4 @@
-// nfs_bases.cuh -- device-side spatial basis, see nfs_bases.cu.
+// nfs_bases.cuh -- device-side input preparation (tables, device bases, S', checks), see nfs_bases.cu.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -9,4 +9,9 @@ cudaError_t launch_spatial_from_grid(const int64_t* d_vox, const double* d_b0, i
                                      const double* fov, int order, double* d_rr, cudaStream_t st);
 cudaError_t launch_col_absmax(const double* d_tab, int64_t n, int nt, unsigned long long* d_out, cudaStream_t st);
 cudaError_t launch_to_float(const double* d_in, float* d_out, int64_t n, cudaStream_t st);
+cudaError_t launch_prep_tables(const double* d_temporal, const double* d_spatial, int64_t K, int64_t L, int p1,
+                               int nt, double* d_tt, double* d_rr, cudaStream_t st);
+cudaError_t launch_prep_sens(const double2* d_sens, const double* d_j, int64_t L, int g, int ldc, bool fp64,
+                             void* d_out, cudaStream_t st);
+cudaError_t launch_count_nonfinite(const double* d_x, int64_t n, unsigned int* d_out, cudaStream_t st);
 }  // namespace nfs

@@ -310,45 +310,83 @@ extern "C" int nfs_plan_attach_comm(nfs_plan* P, const void* uid, int32_t rank, 
 }
 
 // ------------------------------------------------------------------ inputs
-extern "C" int nfs_set_tables(nfs_plan* P, const double* temporal, const double* spatial) {
-  if (!P || (!temporal && P->K > 0) || !spatial) return fail(NFS_ERR_INVALID, "null table");
-  NFS_CUDA(cudaSetDevice(P->device));
-  const int nt = P->NT, p1 = P->P1;
-  const double inv2pi = 1.0 / 6.283185307179586476925286766559;
-  std::vector<double> tt((size_t)P->K * nt, 0.0), rr((size_t)P->L * nt, 0.0);
-  for (int64_t k = 0; k < P->K; ++k)
-    for (int p = 0; p < p1; ++p) tt[(size_t)k * nt + p] = temporal[(size_t)k * p1 + p] * inv2pi;
-  for (int p = 0; p < p1; ++p)
-    for (int64_t l = 0; l < P->L; ++l) rr[(size_t)l * nt + p] = spatial[(size_t)p * P->L + l];
+// FP64 device tables tt [K][nt] (turns) and rr [L][nt] -> the plan's operator tables, the
+// tensor-core images, and the int8-phase fixed-point scales (all on the device)
+static int finish_tables(nfs_plan* P, const double* d_tt, const double* d_rr) {
+  const int nt = P->NT;
+  const int64_t K = P->K, L = P->L;
   if (P->esz == 8) {
-    NFS_CUDA(cudaMemcpyAsync(P->d_T, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice, P->stream));
-    NFS_CUDA(cudaMemcpyAsync(P->d_R, rr.data(), rr.size() * 8, cudaMemcpyHostToDevice, P->stream));
-    NFS_CUDA(cudaStreamSynchronize(P->stream));
+    NFS_CUDA(cudaMemcpyAsync(P->d_T, d_tt, (size_t)K * nt * 8, cudaMemcpyDeviceToDevice, P->stream));
+    NFS_CUDA(cudaMemcpyAsync(P->d_R, d_rr, (size_t)L * nt * 8, cudaMemcpyDeviceToDevice, P->stream));
   } else {
-    std::vector<float> tf(tt.begin(), tt.end()), rf(rr.begin(), rr.end());
-    NFS_CUDA(cudaMemcpyAsync(P->d_T, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice, P->stream));
-    NFS_CUDA(cudaMemcpyAsync(P->d_R, rf.data(), rf.size() * 4, cudaMemcpyHostToDevice, P->stream));
-    NFS_CUDA(cudaStreamSynchronize(P->stream));
+    NFS_CUDA(nfs::launch_to_float(d_tt, (float*)P->d_T, K * nt, P->stream));
+    NFS_CUDA(nfs::launch_to_float(d_rr, (float*)P->d_R, L * nt, P->stream));
   }
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
   P->have_tables = true;
   if (P->tc) {
-    int s = nfs::tc_set_tables(P->tc, P->d_T, P->d_R, P->stream);
-    if (s) return fail(NFS_ERR_CUDA, "tc tables: " + std::string(nfs::tc_last_error()));
+    int st = nfs::tc_set_tables(P->tc, P->d_T, P->d_R, P->stream);
+    if (st) return fail(NFS_ERR_CUDA, "tc tables: " + std::string(nfs::tc_last_error()));
   }
   if (P->tci) {
-    int s = nfs::tci_set_tables(P->tci, tt.data(), rr.data(), P->stream);
-    if (s == 2) {
+    unsigned long long* d_max = nullptr;
+    std::vector<unsigned long long> mx(2 * nt, 0ull);
+    NFS_CUDA(nfs::dev_alloc((void**)&d_max, 2 * nt * sizeof(unsigned long long)));
+    cudaError_t e = nfs::launch_col_absmax(d_tt, K, nt, d_max, P->stream);
+    if (e == cudaSuccess) e = nfs::launch_col_absmax(d_rr, L, nt, d_max + nt, P->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(mx.data(), d_max, 2 * nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, P->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
+    nfs::dev_free(d_max);
+    if (e != cudaSuccess) return fail(NFS_ERR_CUDA, std::string("table maxima: ") + cudaGetErrorString(e));
+    std::vector<double> amax(2 * nt);
+    for (int p = 0; p < 2 * nt; ++p) memcpy(&amax[p], &mx[p], 8);
+    int st = nfs::tci_set_tables_dev(P->tci, d_tt, d_rr, amax.data(), amax.data() + nt, P->stream);
+    if (st == 2) {
       // the exact int8 phase cannot represent this basis (some |t'_p r_p| > 2^12 turns): run
       // the plan on the FP32 CUDA-core contraction instead (same buffers, same results within
       // the FP32 tolerance) and say so in the description
       nfs::tci_destroy(P->tci);
       P->tci = nullptr;
       P->desc += " [f16x3 unavailable for this basis (phase range): FP32 CUDA-core contraction]";
-    } else if (s) {
+    } else if (st) {
       return fail(NFS_ERR_INVALID, "tci tables: " + std::string(nfs::tci_last_error()));
     }
   }
   return NFS_OK;
+}
+
+// scratch device buffers freed on scope exit (after a stream sync)
+struct DevScratch {
+  cudaStream_t st;
+  std::vector<void*> bufs;
+  ~DevScratch() {
+    cudaStreamSynchronize(st);
+    for (void* b : bufs) nfs::dev_free(b);
+  }
+  template <typename T>
+  cudaError_t get(T** p, size_t bytes) {
+    cudaError_t e = nfs::dev_alloc((void**)p, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess) bufs.push_back(*p);
+    return e;
+  }
+};
+
+extern "C" int nfs_set_tables(nfs_plan* P, const double* temporal, const double* spatial) {
+  if (!P || (!temporal && P->K > 0) || !spatial) return fail(NFS_ERR_INVALID, "null table");
+  NFS_CUDA(cudaSetDevice(P->device));
+  const int nt = P->NT, p1 = P->P1;
+  const int64_t K = P->K, L = P->L;
+  // raw tables up, scaling / transposition / padding on the device
+  DevScratch sc{P->stream, {}};
+  double *d_temp = nullptr, *d_spat = nullptr, *d_tt = nullptr, *d_rr = nullptr;
+  NFS_CUDA(sc.get(&d_temp, (size_t)K * p1 * 8));
+  NFS_CUDA(sc.get(&d_spat, (size_t)p1 * L * 8));
+  NFS_CUDA(sc.get(&d_tt, (size_t)K * nt * 8));
+  NFS_CUDA(sc.get(&d_rr, (size_t)L * nt * 8));
+  if (K > 0) NFS_CUDA(cudaMemcpyAsync(d_temp, temporal, (size_t)K * p1 * 8, cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(cudaMemcpyAsync(d_spat, spatial, (size_t)p1 * L * 8, cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(nfs::launch_prep_tables(d_temp, d_spat, K, L, p1, nt, d_tt, d_rr, P->stream));
+  return finish_tables(P, d_tt, d_rr);
 }
 
 // Spatial table evaluated on the device from the masked voxel indices: same
@@ -371,93 +409,37 @@ extern "C" int nfs_set_tables_grid(nfs_plan* P, const double* temporal, const in
   NFS_CUDA(cudaSetDevice(P->device));
   const int nt = P->NT, p1 = P->P1;
   const int64_t K = P->K, L = P->L;
-  const double inv2pi = 1.0 / 6.283185307179586476925286766559;
-  std::vector<double> tt((size_t)K * nt, 0.0), amax_t(nt, 0.0), amax_r(nt, 0.0);
-  for (int64_t k = 0; k < K; ++k)
-    for (int p = 0; p < p1; ++p) {
-      tt[(size_t)k * nt + p] = temporal[(size_t)k * p1 + p] * inv2pi;
-      amax_t[p] = std::max(amax_t[p], std::fabs(tt[(size_t)k * nt + p]));
-    }
+  DevScratch sc{P->stream, {}};
   int64_t* d_vox = nullptr;
-  double *d_b0 = nullptr, *d_rr = nullptr, *d_tt = nullptr;
-  unsigned long long* d_max = nullptr;
-  auto cleanup = [&]() {
-    cudaStreamSynchronize(P->stream);
-    nfs::dev_free(d_vox); nfs::dev_free(d_b0); nfs::dev_free(d_rr); nfs::dev_free(d_tt); nfs::dev_free(d_max);
-  };
-  cudaError_t e = nfs::dev_alloc((void**)&d_vox, std::max<size_t>(L * 8, 8));
-  if (e == cudaSuccess) e = nfs::dev_alloc((void**)&d_b0, std::max<size_t>(L * 8, 8));
-  if (e == cudaSuccess) e = nfs::dev_alloc((void**)&d_rr, std::max<size_t>((size_t)L * nt * 8, 8));
-  if (e == cudaSuccess) e = nfs::dev_alloc((void**)&d_max, nt * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_vox, vox_index, L * 8, cudaMemcpyHostToDevice, P->stream);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_b0, b0_masked, L * 8, cudaMemcpyHostToDevice, P->stream);
-  if (e == cudaSuccess) e = nfs::launch_spatial_from_grid(d_vox, d_b0, L, nt, dims, fov, order, d_rr, P->stream);
-  if (e == cudaSuccess) {
-    if (P->esz == 8) {
-      e = cudaMemcpyAsync(P->d_T, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice, P->stream);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(P->d_R, d_rr, (size_t)L * nt * 8, cudaMemcpyDeviceToDevice, P->stream);
-    } else {
-      std::vector<float> tf(tt.begin(), tt.end());
-      e = cudaMemcpyAsync(P->d_T, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice, P->stream);
-      if (e == cudaSuccess) e = nfs::launch_to_float(d_rr, (float*)P->d_R, (int64_t)L * nt, P->stream);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);   // tf goes out of scope
-    }
-  }
-  if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
-  if (e != cudaSuccess) {
-    cleanup();
-    return fail(NFS_ERR_CUDA, std::string("device bases: ") + cudaGetErrorString(e));
-  }
-  P->have_tables = true;
-  if (P->tc) {
-    int st = nfs::tc_set_tables(P->tc, P->d_T, P->d_R, P->stream);
-    if (st) { cleanup(); return fail(NFS_ERR_CUDA, "tc tables: " + std::string(nfs::tc_last_error())); }
-  }
-  if (P->tci) {
-    std::vector<unsigned long long> mx(nt, 0ull);
-    e = nfs::launch_col_absmax(d_rr, L, nt, d_max, P->stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(mx.data(), d_max, nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, P->stream);
-    if (e == cudaSuccess) e = nfs::dev_alloc((void**)&d_tt, std::max<size_t>(tt.size() * 8, 8));
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_tt, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice, P->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
-    if (e != cudaSuccess) { cleanup(); return fail(NFS_ERR_CUDA, std::string("device bases: ") + cudaGetErrorString(e)); }
-    for (int p = 0; p < nt; ++p) {
-      long long bits = (long long)mx[p];
-      memcpy(&amax_r[p], &bits, 8);
-    }
-    int st = nfs::tci_set_tables_dev(P->tci, d_tt, d_rr, amax_t.data(), amax_r.data(), P->stream);
-    if (st == 2) {
-      nfs::tci_destroy(P->tci);
-      P->tci = nullptr;
-      P->desc += " [f16x3 unavailable for this basis (phase range): FP32 CUDA-core contraction]";
-    } else if (st) {
-      cleanup();
-      return fail(NFS_ERR_INVALID, "tci tables: " + std::string(nfs::tci_last_error()));
-    }
-  }
-  cleanup();
-  return NFS_OK;
+  double *d_b0 = nullptr, *d_temp = nullptr, *d_tt = nullptr, *d_rr = nullptr;
+  NFS_CUDA(sc.get(&d_vox, (size_t)L * 8));
+  NFS_CUDA(sc.get(&d_b0, (size_t)L * 8));
+  NFS_CUDA(sc.get(&d_temp, (size_t)K * p1 * 8));
+  NFS_CUDA(sc.get(&d_tt, (size_t)K * nt * 8));
+  NFS_CUDA(sc.get(&d_rr, (size_t)L * nt * 8));
+  NFS_CUDA(cudaMemcpyAsync(d_vox, vox_index, L * 8, cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(cudaMemcpyAsync(d_b0, b0_masked, L * 8, cudaMemcpyHostToDevice, P->stream));
+  if (K > 0) NFS_CUDA(cudaMemcpyAsync(d_temp, temporal, (size_t)K * p1 * 8, cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(nfs::launch_prep_tables(d_temp, nullptr, K, 0, p1, nt, d_tt, nullptr, P->stream));
+  NFS_CUDA(nfs::launch_spatial_from_grid(d_vox, d_b0, L, nt, dims, fov, order, d_rr, P->stream));
+  return finish_tables(P, d_tt, d_rr);
 }
 
 extern "C" int nfs_set_sens(nfs_plan* P, const double* sens, const double* intensity) {
   if (!P || !sens) return fail(NFS_ERR_INVALID, "null sensitivities");
   NFS_CUDA(cudaSetDevice(P->device));
-  std::vector<double> s2((size_t)P->L * P->ldc * 2, 0.0);
-  for (int64_t l = 0; l < P->L; ++l) {
-    const double j = intensity ? intensity[l] : 1.0;
-    for (int c = 0; c < P->G; ++c) {
-      s2[((size_t)l * P->ldc + c) * 2 + 0] = sens[((size_t)l * P->G + c) * 2 + 0] * j;
-      s2[((size_t)l * P->ldc + c) * 2 + 1] = sens[((size_t)l * P->G + c) * 2 + 1] * j;
-    }
+  const int64_t L = P->L;
+  DevScratch sc{P->stream, {}};
+  double2* d_sens = nullptr;
+  double* d_j = nullptr;
+  NFS_CUDA(sc.get(&d_sens, (size_t)L * P->G * sizeof(double2)));
+  NFS_CUDA(cudaMemcpyAsync(d_sens, sens, (size_t)L * P->G * sizeof(double2), cudaMemcpyHostToDevice, P->stream));
+  if (intensity) {
+    NFS_CUDA(sc.get(&d_j, (size_t)L * 8));
+    NFS_CUDA(cudaMemcpyAsync(d_j, intensity, (size_t)L * 8, cudaMemcpyHostToDevice, P->stream));
   }
-  if (P->esz == 8) {
-    NFS_CUDA(cudaMemcpyAsync(P->d_S, s2.data(), s2.size() * 8, cudaMemcpyHostToDevice, P->stream));
-    NFS_CUDA(cudaStreamSynchronize(P->stream));
-  } else {
-    std::vector<float> sf(s2.begin(), s2.end());
-    NFS_CUDA(cudaMemcpyAsync(P->d_S, sf.data(), sf.size() * 4, cudaMemcpyHostToDevice, P->stream));
-    NFS_CUDA(cudaStreamSynchronize(P->stream));
-  }
+  NFS_CUDA(nfs::launch_prep_sens(d_sens, d_j, L, P->G, P->ldc, P->esz == 8, P->d_S, P->stream));   // S' = S o j
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
   P->have_sens = true;
   if (P->tc) {
     int s = nfs::tc_set_sens(P->tc, P->d_S, P->ldc, P->stream);
@@ -480,11 +462,17 @@ static int upload_samples(nfs_plan* P, const double* sigma, void* dst) {
 
 extern "C" int nfs_set_samples(nfs_plan* P, const double* sigma) {
   if (!P || (!sigma && P->K > 0)) return fail(NFS_ERR_INVALID, "null samples");
-  const size_t n = (size_t)P->K * P->G * 2;
-  for (size_t i = 0; i < n; ++i)
-    if (!isfinite(sigma[i])) return fail(NFS_ERR_NONFINITE, "raw data contains non-finite values");
   NFS_CUDA(cudaSetDevice(P->device));
-  NFS_TRY(upload_samples(P, sigma, P->d_sig));
+  const size_t n = (size_t)P->K * P->G;
+  NFS_TRY(ensure_io(P, std::max<size_t>(n, (size_t)P->L)));
+  NFS_CUDA(cudaMemcpyAsync(P->d_io, sigma, n * sizeof(double2), cudaMemcpyHostToDevice, P->stream));
+  unsigned int bad = 0;
+  unsigned int* d_bad = reinterpret_cast<unsigned int*>(P->d_partials);   // reduction scratch
+  NFS_CUDA(nfs::launch_count_nonfinite(reinterpret_cast<const double*>(P->d_io), (int64_t)n * 2, d_bad, P->stream));
+  NFS_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, P->stream));
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
+  if (bad) return fail(NFS_ERR_NONFINITE, "raw data contains non-finite values");
+  NFS_CUDA(nfs::launch_pack(P->prec == NFS_PREC_FP64 ? 1 : 0, P->d_io, P->d_sig, P->K, P->G, P->ldc, P->stream));
   NFS_CUDA(cudaStreamSynchronize(P->stream));
   P->have_samples = true;
   return NFS_OK;
