@@ -87,6 +87,14 @@ int nfs_set_samples(nfs_plan* plan, const double* sigma);
 int nfs_set_rmse_reference(nfs_plan* plan, const double* ref_masked, const double* weight,
                            double outside_sq, double ref_sq);
 int nfs_rmse_log(nfs_plan* plan, double* out, int32_t n);
+/* Same for the mean SSIM (nfs/metrics.py:20-70) of |rho o j| scattered to an nx x ny image
+ * (x fastest) against ref_img: vox_index = grid index of each reconstructed voxel, weight = j,
+ * kern = the win x win Gaussian window, c1 / c2 from the reference's dynamic range, sel = optional
+ * selection of the (nx-win+1) x (ny-win+1) valid windows.  ref_img == NULL turns it off. */
+int nfs_set_ssim_reference(nfs_plan* plan, const int64_t* vox_index, const double* weight, int32_t nx,
+                           int32_t ny, const double* ref_img, const double* kern, int32_t win, double c1,
+                           double c2, const uint8_t* sel);
+int nfs_ssim_log(nfs_plan* plan, double* out, int32_t n);
 
 /* Operators with host buffers (copies inside).  nfs/engine.py:98-108. */
 int nfs_apply_E(nfs_plan* plan, const double* p, double* y);

@@ -254,3 +254,46 @@ def recon_split(sigma, spatial, temporal, sens, intensity, n_iter, block_starts,
     rho = _cg(p0, lambda v: split_normal_apply(v, s_eff, spatial, temporal, starts),
               n_iter, log, callback)
     return rho, log
+
+
+# ------------------------------------------------------------------ diagnostics
+def gaussian_window(size=11, sigma=1.5):
+    """Truncated, normalised 2D Gaussian window.  nfs/metrics.py:11-17."""
+    half = (size - 1) / 2.0
+    ax = np.arange(size) - half
+    g = np.exp(-(ax ** 2) / (2 * sigma ** 2))
+    k = np.outer(g, g)
+    return k / k.sum()
+
+
+def ssim(test, ref, window=11, sigma=1.5, k1=0.01, k2=0.03, mask=None):
+    """Mean SSIM and map over all windows that fit; dynamic range from ref.  nfs/metrics.py:20-70
+    (direct loops over window positions -- a restatement, not the sliding-window code)."""
+    test, ref = np.asarray(test, float), np.asarray(ref, float)
+    drange = float(ref.max() - ref.min())
+    c1, c2 = (k1 * drange) ** 2, (k2 * drange) ** 2
+    kern = gaussian_window(window, sigma)
+    h0, w0 = test.shape[0] - window + 1, test.shape[1] - window + 1
+    smap = np.empty((h0, w0))
+    for i in range(h0):
+        for j in range(w0):
+            a, b = test[i:i + window, j:j + window], ref[i:i + window, j:j + window]
+            mu1, mu2 = np.sum(kern * a), np.sum(kern * b)
+            v1 = np.sum(kern * a * a) - mu1 ** 2
+            v2 = np.sum(kern * b * b) - mu2 ** 2
+            cov = np.sum(kern * a * b) - mu1 * mu2
+            smap[i, j] = ((2 * mu1 * mu2 + c1) * (2 * cov + c2)) / ((mu1 ** 2 + mu2 ** 2 + c1) * (v1 + v2 + c2))
+    if mask is not None:
+        half = (window - 1) // 2
+        sel = np.asarray(mask, bool)[half:half + h0, half:half + w0]
+        return float(smap[sel].mean()), smap
+    return float(smap.mean()), smap
+
+
+def rmse(test, ref, mask=None):
+    """||test - ref|| / ||ref|| (RMS) over the mask.  nfs/metrics.py:73-88."""
+    test, ref = np.asarray(test).reshape(-1), np.asarray(ref).reshape(-1)
+    if mask is not None:
+        m = np.asarray(mask, bool).reshape(-1)
+        test, ref = test[m], ref[m]
+    return float(np.sqrt(np.mean(np.abs(test - ref) ** 2)) / np.sqrt(np.mean(np.abs(ref) ** 2)))

@@ -9,6 +9,7 @@ from .core import Grid, ReconImage, grid_coordinates
 from .engine import (
     CGLog,
     DeviceRMSE,
+    DeviceSSIM,
     DeviceSpatial,
     EncodingInputs,
     EngineError,
@@ -23,7 +24,7 @@ from .engine import (
 )
 
 __all__ = [
-    "CGLog", "DeviceRMSE", "DeviceSpatial", "EncodingInputs", "EngineError", "Grid", "MemoryBudgetError", "ReconImage",
+    "CGLog", "DeviceRMSE", "DeviceSSIM", "DeviceSpatial", "EncodingInputs", "EngineError", "Grid", "MemoryBudgetError", "ReconImage",
     "apply_E", "apply_EH", "build_bases", "choose_block_starts", "grid_coordinates",
     "phase_block", "recon_full", "recon_split",
 ]

@@ -50,6 +50,10 @@ SIGNATURES = {
     "nfs_apply_EHE_resident": (_c_i32, [_c_void_p, _c_i32]),
     "nfs_set_rmse_reference": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p, ctypes.c_double, ctypes.c_double]),
     "nfs_rmse_log": (_c_i32, [_c_void_p, _c_dbl_p, _c_i32]),
+    "nfs_set_ssim_reference": (_c_i32, [_c_void_p, ctypes.POINTER(_c_i64), _c_dbl_p, _c_i32, _c_i32, _c_dbl_p,
+                                        _c_dbl_p, _c_i32, ctypes.c_double, ctypes.c_double,
+                                        ctypes.POINTER(ctypes.c_uint8)]),
+    "nfs_ssim_log": (_c_i32, [_c_void_p, _c_dbl_p, _c_i32]),
     "nfs_kernel_times": (_c_i32, [_c_void_p, _c_i32, ctypes.POINTER(ctypes.c_float)]),
     "nfs_launches_per_apply": (_c_i32, [_c_void_p]),
     "nfs_plan_describe": (ctypes.c_char_p, [_c_void_p]),
@@ -233,6 +237,29 @@ class Plan:
         w = np.ascontiguousarray(weight, dtype=np.float64).reshape(l)
         _check(self._lib.nfs_set_rmse_reference(self._h, _dp(r.view(np.float64)), _dp(w),
                                                 float(outside_sq), float(ref_sq)))
+
+    def set_ssim_reference(self, vox_index, weight, nx, ny, ref_img, kern, c1, c2, sel=None):
+        """Device per-iteration SSIM diagnostic; ref_img None switches it off."""
+        _, l, _, _ = self.shape
+        if ref_img is None:
+            _check(self._lib.nfs_set_ssim_reference(self._h, None, None, 0, 0, None, None, 0, 0.0, 0.0, None))
+            return
+        v = np.ascontiguousarray(vox_index, dtype=np.int64).reshape(l)
+        w = np.ascontiguousarray(weight, dtype=np.float64).reshape(l)
+        r = np.ascontiguousarray(ref_img, dtype=np.float64).reshape(-1)
+        k = np.ascontiguousarray(kern, dtype=np.float64)
+        sp = None
+        if sel is not None:
+            sel = np.ascontiguousarray(sel, dtype=np.uint8).reshape(-1)
+            sp = sel.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+        _check(self._lib.nfs_set_ssim_reference(self._h, v.ctypes.data_as(ctypes.POINTER(_c_i64)), _dp(w),
+                                                int(nx), int(ny), _dp(r), _dp(k), int(k.shape[0]),
+                                                float(c1), float(c2), sp))
+
+    def ssim_log(self, n: int):
+        out = np.zeros(max(int(n), 1))
+        _check(self._lib.nfs_ssim_log(self._h, _dp(out), int(n)))
+        return out[:int(n)].tolist()
 
     def rmse_log(self, n: int):
         out = np.zeros(max(int(n), 1))

@@ -116,6 +116,13 @@ struct nfs_plan {
   double rmse_outside = 0.0, rmse_ref_sq = 0.0;
   int rmse_cap = 0;
   bool rmse_on = false;
+  // device SSIM diagnostic (nfs_set_ssim_reference)
+  int64_t* d_ssim_vox = nullptr;
+  double *d_ssim_w = nullptr, *d_ssim_img = nullptr, *d_ssim_ref = nullptr, *d_ssim_kern = nullptr, *d_ssim_log = nullptr;
+  unsigned char* d_ssim_sel = nullptr;
+  int ssim_nx = 0, ssim_ny = 0, ssim_win = 0, ssim_cap = 0;
+  double ssim_c1 = 0, ssim_c2 = 0, ssim_nsel = 0;
+  bool ssim_on = false;
 };
 
 static size_t t2size(const nfs_plan* P) { return 2 * P->esz; }
@@ -273,7 +280,9 @@ extern "C" void nfs_plan_destroy(nfs_plan* P) {
   if (P->tci) nfs::tci_destroy(P->tci);
   void* bufs[] = {P->d_T, P->d_R, P->d_S, P->d_sig, P->d_y, P->d_w, P->d_party, P->d_partq,
                   P->d_p, P->d_q, P->d_r, P->d_rho, P->d_q0, P->d_io, P->d_partials,
-                  P->d_cg, P->d_res, P->d_sol, P->d_rmse_ref, P->d_rmse_w, P->d_rmse_log};
+                  P->d_cg, P->d_res, P->d_sol, P->d_rmse_ref, P->d_rmse_w, P->d_rmse_log,
+                  P->d_ssim_vox, P->d_ssim_w, P->d_ssim_img, P->d_ssim_ref, P->d_ssim_kern, P->d_ssim_log,
+                  P->d_ssim_sel};
   for (void* b : bufs)
     if (b) nfs::dev_free(b);
   if (P->comm && nccl_api().ok) nccl_api().destroy(P->comm);
@@ -617,6 +626,63 @@ static int cg_iteration(nfs_plan* P) {
   if (P->rmse_on)
     NFS_CUDA(nfs::launch_cg_rmse(P->d_rho, P->d_rmse_ref, P->d_rmse_w, P->L, P->d_cg, P->d_partials,
                                  P->rmse_outside, P->rmse_ref_sq, P->d_rmse_log, P->stream));
+  if (P->ssim_on)
+    NFS_CUDA(nfs::launch_cg_ssim(P->d_rho, P->d_ssim_w, P->d_ssim_vox, P->L, P->d_ssim_img, P->d_ssim_ref,
+                                 P->ssim_nx, P->ssim_ny, P->d_ssim_kern, P->ssim_win, P->ssim_c1, P->ssim_c2,
+                                 P->d_ssim_sel, P->ssim_nsel, P->d_cg, P->d_partials, P->d_ssim_log, P->stream));
+  return NFS_OK;
+}
+
+// Device-side per-iteration mean SSIM of |rho o j| on an nx x ny grid against
+// ref_img (nx*ny, x fastest), window kernel kern (win x win), constants c1, c2 (from the
+// reference's dynamic range), optional window selection sel ((nx-win+1) x (ny-win+1), x
+// fastest).  vox_index: grid index of every reconstructed voxel; weight: j.  NULL ref_img off.
+extern "C" int nfs_set_ssim_reference(nfs_plan* P, const int64_t* vox_index, const double* weight, int32_t nx,
+                                      int32_t ny, const double* ref_img, const double* kern, int32_t win,
+                                      double c1, double c2, const uint8_t* sel) {
+  if (!P) return fail(NFS_ERR_INVALID, "null plan");
+  if (!ref_img) {
+    P->ssim_on = false;
+    return NFS_OK;
+  }
+  if (!vox_index || !weight || !kern || nx < win || ny < win || win < 1)
+    return fail(NFS_ERR_INVALID, "image smaller than the SSIM window");
+  const int64_t npix = (int64_t)nx * ny, nwin = (int64_t)(nx - win + 1) * (ny - win + 1);
+  for (int64_t l = 0; l < P->L; ++l)
+    if (vox_index[l] < 0 || vox_index[l] >= npix) return fail(NFS_ERR_INVALID, "voxel index outside the image");
+  double n_sel = (double)nwin;
+  if (sel) {
+    n_sel = 0;
+    for (int64_t o = 0; o < nwin; ++o) n_sel += sel[o] ? 1.0 : 0.0;
+    if (n_sel == 0) return fail(NFS_ERR_INVALID, "mask covers no valid windows");
+  }
+  NFS_CUDA(cudaSetDevice(P->device));
+  cudaStreamSynchronize(P->stream);
+  void* old[] = {P->d_ssim_vox, P->d_ssim_w, P->d_ssim_img, P->d_ssim_ref, P->d_ssim_kern, P->d_ssim_sel};
+  for (void* b : old) nfs::dev_free(b);
+  P->d_ssim_vox = nullptr; P->d_ssim_w = P->d_ssim_img = P->d_ssim_ref = P->d_ssim_kern = nullptr;
+  P->d_ssim_sel = nullptr;
+  NFS_CUDA(nfs::dev_alloc((void**)&P->d_ssim_vox, std::max<int64_t>(P->L, 1) * 8));
+  NFS_CUDA(nfs::dev_alloc((void**)&P->d_ssim_w, std::max<int64_t>(P->L, 1) * 8));
+  NFS_CUDA(nfs::dev_alloc((void**)&P->d_ssim_img, npix * 8));
+  NFS_CUDA(nfs::dev_alloc((void**)&P->d_ssim_ref, npix * 8));
+  NFS_CUDA(nfs::dev_alloc((void**)&P->d_ssim_kern, (size_t)win * win * 8));
+  if (sel) NFS_CUDA(nfs::dev_alloc((void**)&P->d_ssim_sel, nwin));
+  NFS_CUDA(cudaMemcpyAsync(P->d_ssim_vox, vox_index, P->L * 8, cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(cudaMemcpyAsync(P->d_ssim_w, weight, P->L * 8, cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(cudaMemcpyAsync(P->d_ssim_ref, ref_img, npix * 8, cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(cudaMemcpyAsync(P->d_ssim_kern, kern, (size_t)win * win * 8, cudaMemcpyHostToDevice, P->stream));
+  if (sel) NFS_CUDA(cudaMemcpyAsync(P->d_ssim_sel, sel, nwin, cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
+  P->ssim_nx = nx; P->ssim_ny = ny; P->ssim_win = win; P->ssim_c1 = c1; P->ssim_c2 = c2; P->ssim_nsel = n_sel;
+  P->ssim_on = true;
+  return NFS_OK;
+}
+
+extern "C" int nfs_ssim_log(nfs_plan* P, double* out, int32_t n) {
+  if (!P || !out || n < 0) return fail(NFS_ERR_INVALID, "bad arguments");
+  if (!P->ssim_on || n > P->ssim_cap) return fail(NFS_ERR_INVALID, "no SSIM log of that length");
+  if (n > 0) NFS_CUDA(cudaMemcpy(out, P->d_ssim_log, n * sizeof(double), cudaMemcpyDeviceToHost));
   return NFS_OK;
 }
 
@@ -671,6 +737,13 @@ extern "C" int nfs_cg_solve(nfs_plan* P, int32_t n_iter, nfs_iter_callback cb, v
     NFS_CUDA(nfs::dev_alloc((void**)&P->d_res, std::max(n_iter, 1) * sizeof(double)));
     NFS_CUDA(nfs::dev_alloc((void**)&P->d_sol, std::max(n_iter, 1) * sizeof(double)));
     P->log_cap = n_iter;
+  }
+  if (P->ssim_on && n_iter > P->ssim_cap) {
+    cudaStreamSynchronize(P->stream);
+    nfs::dev_free(P->d_ssim_log);
+    P->d_ssim_log = nullptr;
+    NFS_CUDA(nfs::dev_alloc((void**)&P->d_ssim_log, std::max(n_iter, 1) * sizeof(double)));
+    P->ssim_cap = n_iter;
   }
   if (P->rmse_on && n_iter > P->rmse_cap) {
     cudaStreamSynchronize(P->stream);

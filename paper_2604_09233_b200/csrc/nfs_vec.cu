@@ -266,6 +266,54 @@ __global__ void cg_rmse_kernel(const double2* __restrict__ rho, const double2* _
 cudaError_t launch_cg_rmse(const double2* rho, const double2* ref, const double* w, int64_t n, CGState* s,
                            double* partials, double outside, double ref_sq, double* log, cudaStream_t st);
 
+// per-iteration mean SSIM of |rho o j| scattered to the 2D grid against a reference image (SURVEY
+// 8f f4; the reference's metrics.ssim, nfs/metrics.py:20-70: Gaussian-weighted local statistics
+// over all windows that fit, dynamic range from the reference, optional window selection).
+__global__ void ssim_scatter_kernel(const double2* __restrict__ rho, const double* __restrict__ w,
+                                    const int64_t* __restrict__ vox, int64_t n, const CGState* st,
+                                    double* __restrict__ img) {
+  if (st->err || st->iter < 1) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 x = rho[i];
+    img[vox[i]] = hypot(x.x * w[i], x.y * w[i]);   // |rho_l j_l|
+  }
+}
+
+__global__ void ssim_eval_kernel(const double* __restrict__ img, const double* __restrict__ ref, int nx, int ny,
+                                 const double* __restrict__ kern, int win, double c1, double c2,
+                                 const unsigned char* __restrict__ sel, double n_sel, CGState* st,
+                                 double* partials, double* log) {
+  if (st->err || st->iter < 1) return;
+  const int ox_n = nx - win + 1, oy_n = ny - win + 1;
+  const int64_t n = (int64_t)ox_n * oy_n;
+  double v[1] = {0.0};
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+    const int ox = (int)(o % ox_n), oy = (int)(o / ox_n);
+    if (sel && !sel[o]) continue;
+    double m1 = 0, m2 = 0, e11 = 0, e22 = 0, e12 = 0;
+    for (int b = 0; b < win; ++b)
+      for (int a = 0; a < win; ++a) {
+        const double k = kern[a * win + b];
+        const int64_t idx = (int64_t)(ox + a) + (int64_t)nx * (oy + b);
+        const double t = img[idx], r = ref[idx];
+        m1 = fma(k, t, m1);
+        m2 = fma(k, r, m2);
+        e11 = fma(k, t * t, e11);
+        e22 = fma(k, r * r, e22);
+        e12 = fma(k, t * r, e12);
+      }
+    const double v1 = e11 - m1 * m1, v2 = e22 - m2 * m2, cov = e12 - m1 * m2;
+    v[0] += ((2 * m1 * m2 + c1) * (2 * cov + c2)) / ((m1 * m1 + m2 * m2 + c1) * (v1 + v2 + c2));
+  }
+  double tot[1];
+  if (grid_sum<1>(v, partials, &st->ticket, tot) && threadIdx.x == 0) log[st->iter - 1] = tot[0] / n_sel;
+}
+
+cudaError_t launch_cg_ssim(const double2* rho, const double* w, const int64_t* vox, int64_t n, double* img,
+                           const double* ref, int nx, int ny, const double* kern, int win, double c1, double c2,
+                           const unsigned char* sel, double n_sel, CGState* s, double* partials, double* log,
+                           cudaStream_t st);
+
 // ------------------------------------------------------------------ phase materialisation
 template <typename T, int NT>
 __global__ void phase_rows_kernel(const T* __restrict__ ttab, const T* __restrict__ rtab,
@@ -346,6 +394,17 @@ cudaError_t launch_cg_iter_tail(const double2* q, double2* p, double2* r, double
 cudaError_t launch_cg_rmse(const double2* rho, const double2* ref, const double* w, int64_t n, CGState* s,
                            double* partials, double outside, double ref_sq, double* log, cudaStream_t st) {
   cg_rmse_kernel<<<cg_grid(n), 256, 0, st>>>(rho, ref, w, n, s, partials, outside, ref_sq, log);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_ssim(const double2* rho, const double* w, const int64_t* vox, int64_t n, double* img,
+                           const double* ref, int nx, int ny, const double* kern, int win, double c1, double c2,
+                           const unsigned char* sel, double n_sel, CGState* s, double* partials, double* log,
+                           cudaStream_t st) {
+  cudaMemsetAsync(img, 0, (size_t)nx * ny * sizeof(double), st);
+  ssim_scatter_kernel<<<cg_grid(n), 256, 0, st>>>(rho, w, vox, n, s, img);
+  const int64_t nw = (int64_t)(nx - win + 1) * (ny - win + 1);
+  ssim_eval_kernel<<<cg_grid(nw), 256, 0, st>>>(img, ref, nx, ny, kern, win, c1, c2, sel, n_sel, s, partials, log);
   return cudaGetLastError();
 }
 

@@ -26,6 +26,10 @@ cudaError_t launch_reduce_parts(int prec, const void* part, void* out, int64_t n
 cudaError_t launch_reduce_image(int prec, const void* part, double2* q, int64_t n, int n_part,
                                 const int* stop, cudaStream_t st);
 int cg_grid(int64_t n);
+cudaError_t launch_cg_ssim(const double2* rho, const double* w, const int64_t* vox, int64_t n, double* img,
+                           const double* ref, int nx, int ny, const double* kern, int win, double c1, double c2,
+                           const unsigned char* sel, double n_sel, CGState* s, double* partials, double* log,
+                           cudaStream_t st);
 cudaError_t launch_cg_rmse(const double2* rho, const double2* ref, const double* w, int64_t n, CGState* s,
                            double* partials, double outside, double ref_sq, double* log, cudaStream_t st);
 cudaError_t launch_cg_init(const double2* q0, double2* r, double2* p, double2* rho, int64_t n,

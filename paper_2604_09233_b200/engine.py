@@ -153,9 +153,9 @@ class DeviceRMSE:
         def cb(n, rho_r):
             full = zeros(L); full[mask_r] = rho_r * j; errs.append(metrics.rmse(full, ref, support))
 
-    Passed as `callback=` to recon_full / recon_split, the relative RMSE of every iterate is
-    evaluated inside the device CG loop (no per-iteration host copy of the iterate) and lands in
-    `.values` when the solve returns (one value per completed iteration).
+    Passed as `callback=` to recon_full / recon_split (alone or in a list with DeviceSSIM), the
+    relative RMSE of every iterate is evaluated inside the device CG loop (no per-iteration host
+    copy of the iterate) and lands in `.values` when the solve returns.
     """
 
     def __init__(self, reference, support=None):
@@ -176,8 +176,72 @@ class DeviceRMSE:
         outside = float(np.sum(np.abs(self.reference[sup & ~mask_r]) ** 2))
         return ref_m, w, outside, ref_sq
 
+    def _attach(self, plan, inputs):
+        plan.set_rmse_reference(*self._restricted(inputs.mask_r, inputs.intensity))
+
+    def _collect(self, plan, n_done):
+        self.values = plan.rmse_log(n_done)
+        plan.set_rmse_reference(None, None, 0.0, 0.0)
+
     def __call__(self, n, rho_r):
         raise EngineError("DeviceRMSE is evaluated on the device by recon_full / recon_split")
+
+
+class DeviceSSIM:
+    """Per-iteration mean SSIM of the magnitude image on the GPU.
+
+    Equivalent to a convergence-study callback computing
+    ``metrics.ssim(abs(full).reshape(nx, ny, order="F"), reference, window, sigma, k1, k2, mask)``
+    (nfs/metrics.py:20-70) with ``full[mask_r] = rho_r * j`` on a 2D grid; the values land in
+    `.values` when the solve returns.
+    """
+
+    def __init__(self, reference, window: int = 11, sigma: float = 1.5, k1: float = 0.01, k2: float = 0.03,
+                 mask=None):
+        self.reference = np.asarray(reference, dtype=float)
+        if self.reference.ndim != 2:
+            raise EngineError("ssim expects a 2D reference image (nx, ny)")
+        nx, ny = self.reference.shape
+        if nx < window or ny < window:
+            raise EngineError(f"image smaller than the {window}x{window} window")
+        drange = float(self.reference.max() - self.reference.min())
+        if drange == 0:
+            raise EngineError("reference image is constant")
+        half = (window - 1) / 2.0
+        ax = np.arange(window) - half
+        g = np.exp(-(ax ** 2) / (2 * sigma ** 2))
+        kern = np.outer(g, g)
+        self.kern = kern / kern.sum()
+        self.window, self.c1, self.c2 = int(window), (k1 * drange) ** 2, (k2 * drange) ** 2
+        self.sel = None
+        if mask is not None:
+            m = np.asarray(mask, dtype=bool).reshape(nx, ny)
+        h = (window - 1) // 2
+        if mask is not None:
+            sel = m[h:h + nx - window + 1, h:h + ny - window + 1]
+            if not sel.any():
+                raise EngineError("mask covers no valid windows")
+            self.sel = sel.reshape(-1, order="F").astype(np.uint8)
+        self.values: list = []
+
+    def _attach(self, plan, inputs):
+        grid = inputs.grid
+        nx, ny = self.reference.shape
+        if grid.dims[2] != 1 or (grid.dims[0], grid.dims[1]) != (nx, ny):
+            raise EngineError("SSIM reference must match the 2D grid")
+        vox = np.flatnonzero(inputs.mask_r).astype(np.int64)
+        plan.set_ssim_reference(vox, np.asarray(inputs.intensity, dtype=float), nx, ny,
+                                self.reference.reshape(-1, order="F"), self.kern, self.c1, self.c2, self.sel)
+
+    def _collect(self, plan, n_done):
+        self.values = plan.ssim_log(n_done)
+        plan.set_ssim_reference(None, None, 0, 0, None, None, 0.0, 0.0)
+
+    def __call__(self, n, rho_r):
+        raise EngineError("DeviceSSIM is evaluated on the device by recon_full / recon_split")
+
+
+_DEVICE_DIAGNOSTICS = (DeviceRMSE, DeviceSSIM)
 
 
 class PhaseBlock:
@@ -316,20 +380,30 @@ def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label:
     return plan
 
 
+def _device_diagnostics(callback):
+    """The device-evaluated diagnostics in `callback` (one object or a list), else ()."""
+    if isinstance(callback, _DEVICE_DIAGNOSTICS):
+        return (callback,)
+    if isinstance(callback, (list, tuple)) and callback and all(isinstance(c, _DEVICE_DIAGNOSTICS) for c in callback):
+        return tuple(callback)
+    return ()
+
+
 def _run_cg(plan, inputs: EncodingInputs, log: CGLog, callback):
-    device_rmse = isinstance(callback, DeviceRMSE)
-    if device_rmse:
-        plan.set_rmse_reference(*callback._restricted(inputs.mask_r, inputs.intensity))
+    diags = _device_diagnostics(callback)
+    for d in diags:
+        d._attach(plan, inputs)
+    if diags:
         callback = None
     rho, res, sol, tim, n_done = plan.cg_solve(inputs.n_iter, callback)
-    if device_rmse:
-        device_rmse = plan.rmse_log(n_done)
+    for d in diags:
+        d._collect(plan, n_done)
     log.add_timing("initial_adjoint", float(tim[0]))
     for n in range(1, n_done + 1):
         log.add_timing(f"cg_iteration_{n}", float(tim[1 + n]))
     log.residual_norms.extend(res)
     log.solution_norms.extend(sol)
-    return rho, device_rmse
+    return rho
 
 
 def _finalize(rho_r: np.ndarray, inputs: EncodingInputs, log: CGLog) -> ReconImage:
@@ -365,9 +439,7 @@ def recon_full(inputs: EncodingInputs, memory_budget_bytes: int | None = None, c
         raise EngineError("raw data contains non-finite values")
     plan = _make_plan(inputs, precision or default_precision(), log, timing_label=True)
     try:
-        rho, rmse_values = _run_cg(plan, inputs, log, callback)
-        if isinstance(callback, DeviceRMSE):
-            callback.values = rmse_values
+        rho = _run_cg(plan, inputs, log, callback)
     finally:
         plan.close()
     return _finalize(rho, inputs, log), log
@@ -386,9 +458,7 @@ def recon_split(inputs: EncodingInputs, callback=None, *, precision: str | None 
         raise EngineError("raw data contains non-finite values")
     plan = _make_plan(inputs, precision or default_precision(), log, timing_label=False)
     try:
-        rho, rmse_values = _run_cg(plan, inputs, log, callback)
-        if isinstance(callback, DeviceRMSE):
-            callback.values = rmse_values
+        rho = _run_cg(plan, inputs, log, callback)
     finally:
         plan.close()
     return _finalize(rho, inputs, log), log

@@ -212,8 +212,27 @@ def case_config_b_rows():
          EH_rows=engine.apply_EH(sig, sens, phase).astype(np.complex128))
 
 
+def case_metrics():
+    """nfs/metrics.py ssim / rmse (tests/test_metrics.py) on the images a convergence study
+    compares: a 24x20 magnitude image vs a reference, with and without a window mask."""
+    from nfsense import metrics
+    rng = np.random.default_rng(13)
+    ref = np.abs(rng.standard_normal((24, 20))) + np.linspace(0, 2, 20)[None, :]
+    test = ref + 0.2 * rng.standard_normal((24, 20))
+    mask = rng.random((24, 20)) < 0.6
+    m_plain, smap_plain = metrics.ssim(test, ref)
+    m_mask, _ = metrics.ssim(test, ref, mask=mask)
+    m_w5, smap_w5 = metrics.ssim(test, ref, window=5, sigma=1.5)
+    full_ref = rng.standard_normal(300) + 1j * rng.standard_normal(300)
+    full_test = full_ref + 0.1 * (rng.standard_normal(300) + 1j * rng.standard_normal(300))
+    sup = rng.random(300) < 0.5
+    save("metrics", ref=ref, test=test, mask=mask, ssim_plain=np.array(m_plain), smap_plain=smap_plain,
+         ssim_mask=np.array(m_mask), ssim_w5=np.array(m_w5), smap_w5=smap_w5, full_ref=full_ref,
+         full_test=full_test, support=sup, rmse=np.array(metrics.rmse(full_test, full_ref, sup)))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["engine8", "oracle_eq", "config_a", "small3d", "cartesian8",
-                             "config_b_rows"]
+                             "config_b_rows", "metrics"]
     for name in which:
         globals()["case_" + name]()

@@ -419,3 +419,38 @@ def test_device_rmse_diagnostic(prec, tol):
     engine.recon_full(inp, callback=dev, precision=prec)
     assert len(dev.values) == len(host) == 12
     assert np.max(np.abs(np.array(dev.values) - np.array(host)) / np.array(host)) < tol
+
+
+@pytest.mark.parametrize("window,use_mask", [(11, False), (5, True)])
+def test_device_ssim_diagnostic(window, use_mask):
+    """DeviceSSIM (with DeviceRMSE in the same solve) logs the per-iteration mean
+    SSIM of |rho o j| inside the device CG loop; equal to oracle.ssim (pinned to the reference's
+    nfs/metrics.py values) evaluated on the host on the same iterates."""
+    rng = np.random.default_rng(31)
+    nx, ny = 20, 18
+    grid = Grid((nx, ny, 1), (0.2, 0.18, 0.002))
+    mask = rng.random(grid.nvox) < 0.8
+    L = int(mask.sum())
+    K, G = 500, 4
+    spatial = rng.standard_normal((3, L)) * 0.5
+    temporal = rng.standard_normal((K, 3)) * 3.0
+    sens = rng.standard_normal((L, G)) + 1j * rng.standard_normal((L, G))
+    j = 0.5 + rng.random(L)
+    sigma = rng.standard_normal((K, G)) + 1j * rng.standard_normal((K, G))
+    ref_img = np.abs(rng.standard_normal((nx, ny))) + 0.5
+    win_mask = (rng.random((nx, ny)) < 0.7) if use_mask else None
+
+    def host_ssim(rho_r):
+        full = np.zeros(grid.nvox, complex)
+        full[mask] = rho_r * j
+        return orc.ssim(np.abs(full).reshape(nx, ny, order="F"), ref_img, window=window, mask=win_mask)[0]
+
+    host = []
+    inp = inputs_from(grid, sigma, spatial, temporal, sens, 8, mask=mask, intensity=j)
+    engine.recon_full(inp, callback=lambda n, r: host.append(host_ssim(r)), precision="fp64")
+    dev = engine.DeviceSSIM(ref_img, window=window, mask=win_mask)
+    dev_rmse = engine.DeviceRMSE(np.zeros(grid.nvox) + 1.0)
+    inp = inputs_from(grid, sigma, spatial, temporal, sens, 8, mask=mask, intensity=j)
+    engine.recon_full(inp, callback=[dev, dev_rmse], precision="fp64")
+    assert len(dev.values) == len(host) == 8 and len(dev_rmse.values) == 8
+    assert np.max(np.abs(np.array(dev.values) - np.array(host))) < 1e-10

@@ -169,3 +169,14 @@ def test_device_rmse_restriction_host_logic():
         engine.DeviceRMSE(np.zeros(n), support)._restricted(mask, j)
     with pytest.raises(engine.EngineError):
         engine.DeviceRMSE(ref, support)(1, rho)
+
+
+def test_oracle_metrics_vs_reference_golden():
+    """oracle.ssim / oracle.rmse (restatements of nfs/metrics.py) pinned to the reference's values."""
+    g = golden("metrics")
+    m, smap = orc.ssim(g["test"], g["ref"])
+    assert abs(m - float(g["ssim_plain"])) < 1e-12 and np.allclose(smap, g["smap_plain"], atol=1e-12)
+    assert abs(orc.ssim(g["test"], g["ref"], mask=g["mask"])[0] - float(g["ssim_mask"])) < 1e-12
+    m5, smap5 = orc.ssim(g["test"], g["ref"], window=5, sigma=1.5)
+    assert abs(m5 - float(g["ssim_w5"])) < 1e-12 and np.allclose(smap5, g["smap_w5"], atol=1e-12)
+    assert abs(orc.rmse(g["full_test"], g["full_ref"], g["support"]) - float(g["rmse"])) < 1e-14
