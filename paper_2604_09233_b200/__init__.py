@@ -20,13 +20,14 @@ from .engine import (
     choose_block_starts,
     phase_block,
     recon_full,
+    recon_slices,
     recon_split,
 )
 
 __all__ = [
     "CGLog", "DeviceRMSE", "DeviceSSIM", "DeviceSpatial", "EncodingInputs", "EngineError", "Grid", "MemoryBudgetError", "ReconImage",
     "apply_E", "apply_EH", "build_bases", "choose_block_starts", "grid_coordinates",
-    "phase_block", "recon_full", "recon_split",
+    "phase_block", "recon_full", "recon_slices", "recon_split",
 ]
 
 __version__ = "0.1.0"

@@ -355,28 +355,34 @@ def _nccl_unique_id(dist, rank):
     return obj[0]
 
 
-def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label: bool):
-    """Create the device plan for this rank's sample shard; upload tables, S', sigma."""
-    dist, rank, world = _dist_info()
+def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label: bool, shard: bool = True):
+    """Create the device plan for this rank's sample shard; upload tables, S', sigma.
+
+    `shard=False` solves the whole problem on this rank (independent slices, recon_slices)."""
+    dist, rank, world = _dist_info() if shard else (None, 0, 1)
     lo, hi = shard_rows(inputs.n_samples, rank, world)
     device = default_device()
     t0 = time.perf_counter()
     plan = _native.Plan(hi - lo, inputs.n_voxels, inputs.sens.shape[1],
                         inputs.spatial.shape[0], precision, device)
-    if world > 1:
-        plan.attach_comm(_nccl_unique_id(dist, rank), rank, world)
-    t_plan = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    plan.set_sens(inputs.sens, inputs.intensity)          # S' = S o j on upload
-    log.add_timing("intensity_correction", time.perf_counter() - t0)
-    t0 = time.perf_counter()
-    if isinstance(inputs.spatial, DeviceSpatial):
-        inputs.spatial.upload(plan, inputs.temporal[lo:hi])
-    else:
-        plan.set_tables(inputs.temporal[lo:hi], inputs.spatial)
-    if timing_label:   # the GPU analogue of building P: plan + table upload
-        log.add_timing("build_phase_matrix", t_plan + time.perf_counter() - t0)
-    plan.set_samples(inputs.sigma[lo:hi])
+    try:
+        if world > 1:
+            plan.attach_comm(_nccl_unique_id(dist, rank), rank, world)
+        t_plan = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        plan.set_sens(inputs.sens, inputs.intensity)          # S' = S o j on upload
+        log.add_timing("intensity_correction", time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        if isinstance(inputs.spatial, DeviceSpatial):
+            inputs.spatial.upload(plan, inputs.temporal[lo:hi])
+        else:
+            plan.set_tables(inputs.temporal[lo:hi], inputs.spatial)
+        if timing_label:   # the GPU analogue of building P: plan + table upload
+            log.add_timing("build_phase_matrix", t_plan + time.perf_counter() - t0)
+        plan.set_samples(inputs.sigma[lo:hi])   # raw data finiteness checked on the device
+    except BaseException:
+        plan.close()
+        raise
     return plan
 
 
@@ -434,15 +440,53 @@ def recon_full(inputs: EncodingInputs, memory_budget_bytes: int | None = None, c
     if memory_budget_bytes is not None and need > memory_budget_bytes:
         raise MemoryBudgetError(
             f"phase matrix needs {need} bytes (> budget {memory_budget_bytes}); use the split variant")
-    log = CGLog()
-    if not np.all(np.isfinite(inputs.sigma)):
+    return _recon_full(inputs, callback, precision, shard=True)
+
+
+def _check_samples(inputs: EncodingInputs, shard: bool):
+    # single rank: nfs_set_samples checks finiteness on the device (same error); sharded: every
+    # rank must fail together before any collective, so check the full array on the host
+    if shard and _dist_info()[2] > 1 and not np.all(np.isfinite(inputs.sigma)):
         raise EngineError("raw data contains non-finite values")
-    plan = _make_plan(inputs, precision or default_precision(), log, timing_label=True)
+
+
+def _recon_full(inputs: EncodingInputs, callback, precision, shard: bool):
+    log = CGLog()
+    _check_samples(inputs, shard)
+    plan = _make_plan(inputs, precision or default_precision(), log, timing_label=True, shard=shard)
     try:
         rho = _run_cg(plan, inputs, log, callback)
     finally:
         plan.close()
     return _finalize(rho, inputs, log), log
+
+
+def recon_slices(inputs_list, memory_budget_bytes: int | None = None, *, precision: str | None = None,
+                 gather: bool = True):
+    """Independent problems (slices of a multi-slice acquisition).
+
+    With torch.distributed initialised, slice i is reconstructed by rank i mod world with no
+    collective in the solve ("replicas" of the solver, not of the data); `gather=True` returns
+    every slice's (ReconImage, CGLog) on every rank (one all_gather of the results), otherwise
+    each rank gets only its own slices (None elsewhere).  Each slice follows recon_full's rules.
+    """
+    dist, rank, world = _dist_info()
+    out = [None] * len(inputs_list)
+    for i, inputs in enumerate(inputs_list):
+        if i % world != rank:
+            continue
+        need = inputs.n_samples * inputs.n_voxels * 16
+        if memory_budget_bytes is not None and need > memory_budget_bytes:
+            raise MemoryBudgetError(
+                f"phase matrix needs {need} bytes (> budget {memory_budget_bytes}); use the split variant")
+        out[i] = _recon_full(inputs, None, precision, shard=False)
+    if gather and world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, {i: r for i, r in enumerate(out) if r is not None})
+        for part in parts:
+            for i, r in part.items():
+                out[i] = r
+    return out
 
 
 def recon_split(inputs: EncodingInputs, callback=None, *, precision: str | None = None):
@@ -454,8 +498,7 @@ def recon_split(inputs: EncodingInputs, callback=None, *, precision: str | None 
     if inputs.block_starts is None:
         raise EngineError("split reconstruction needs block starts")
     log = CGLog()
-    if not np.all(np.isfinite(inputs.sigma)):
-        raise EngineError("raw data contains non-finite values")
+    _check_samples(inputs, True)
     plan = _make_plan(inputs, precision or default_precision(), log, timing_label=False)
     try:
         rho = _run_cg(plan, inputs, log, callback)

@@ -67,3 +67,41 @@ def test_sample_sharded_cg_matches_single_process(tmp_path, world):
     assert np.linalg.norm(rhos[0] - ref) / np.linalg.norm(ref) < 1e-10
     assert np.allclose(np.load(tmp_path / "res0.npy"), ref_log.residual_norms, rtol=1e-8)
     assert np.allclose(rhos[0], g["full_values"], atol=1e-10)
+
+
+def _slices_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_09233_b200 import engine
+
+    calls = []
+
+    def fake_recon(inputs, callback, precision, shard):   # the GPU solve, replaced on CPU
+        assert shard is False and callback is None
+        calls.append(int(inputs))
+        return ("image", int(inputs), rank), ("log", int(inputs))
+
+    engine._recon_full = fake_recon
+    n = 7
+
+    class Fake(int):   # stands in for EncodingInputs (size checks only)
+        n_samples, n_voxels = 3, 5
+
+    out = engine.recon_slices([Fake(i) for i in range(n)])
+    np.save(os.path.join(out_dir, f"slices{rank}.npy"),
+            np.array([[r[0][1], r[0][2], r[1][1]] for r in out]))
+    np.save(os.path.join(out_dir, f"calls{rank}.npy"), np.array(calls))
+    dist.destroy_process_group()
+
+
+def test_recon_slices_replicas_without_collective(tmp_path):
+    """slice i is solved on rank i mod world (no collective in the solve)
+    and every rank receives all results in slice order."""
+    world = 2
+    port = _free_port()
+    mp.spawn(_slices_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        got = np.load(tmp_path / f"slices{r}.npy")
+        assert np.array_equal(got[:, 0], np.arange(7)) and np.array_equal(got[:, 2], np.arange(7))
+        assert np.array_equal(got[:, 1], np.arange(7) % world)      # solved by rank i mod world
+        assert np.array_equal(np.load(tmp_path / f"calls{r}.npy"), np.arange(r, 7, world))

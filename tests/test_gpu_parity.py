@@ -454,3 +454,15 @@ def test_device_ssim_diagnostic(window, use_mask):
     engine.recon_full(inp, callback=[dev, dev_rmse], precision="fp64")
     assert len(dev.values) == len(host) == 8 and len(dev_rmse.values) == 8
     assert np.max(np.abs(np.array(dev.values) - np.array(host))) < 1e-10
+
+
+def test_recon_slices_single_rank_matches_recon_full():
+    """recon_slices on one rank = recon_full per slice (bitwise, fp64)."""
+    g = golden("engine8")
+    grid = Grid((8, 8, 1), (0.08, 0.08, 0.002))
+    slices = [inputs_from(grid, g["sigma"] * (1 + 0.1 * i), g["spatial"], g["temporal"], g["sens"], 6)
+              for i in range(3)]
+    out = engine.recon_slices(slices, precision="fp64")
+    for i, (img, log) in enumerate(out):
+        ref, _ = engine.recon_full(slices[i], precision="fp64")
+        assert np.array_equal(img.values, ref.values) and len(log.residual_norms) == 6
