@@ -53,6 +53,13 @@ constexpr int SEG = NFS_TC_SEG; // chunks accumulated in one TMEM D buffer befor
 constexpr int GPQ = 2;          // generator warps per TMEM lane quadrant (chunk c -> warp c % GPQ)
 constexpr int GEN_WARPS = 4 * GPQ;
 constexpr int THREADS = (GEN_WARPS + 2) * 32;
+#ifndef NFS_TC_DEBUG
+#define NFS_TC_DEBUG 0
+#endif
+// profiling builds only (-DNFS_TC_DEBUG=m): bit0 skip the phasor math, bit1 skip the MMAs,
+// bit2 skip the TMEM stores, bit3 skip the bulk copies; compile-time so the product kernel
+// carries no runtime branch in its inner loops
+constexpr int TC_DEBUG = NFS_TC_DEBUG;
 constexpr int CTAS_PER_SM = 2;
 constexpr int TMEM_COLS = 512 / CTAS_PER_SM;  // D0 [0,64) D1 [64,128) A stages [128, TMEM_COLS)
 constexpr int A_COL0 = 128;
@@ -230,7 +237,7 @@ struct Args {
   const float* scale;     // [1] B scale of this call (F16), device
   float2* out;            // fwd: partial y [split][K][ldc]; adj: partial q [group*split+split][L]
   const int* stop;
-  int debug;              // profiling only: bit0 skip A math, bit1 skip MMAs
+  int unused_debug;       // (profiling switches are compile-time: NFS_TC_DEBUG)
   long long* trace;       // profiling only: per-chunk timestamps of CTA (0,0), or null
 };
 
@@ -325,7 +332,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
         uint32_t hi[NV], lo[NV];
-        if (a.debug & 1) {
+        if (TC_DEBUG & 1) {
 #pragma unroll
           for (int i = 0; i < NV; ++i) { hi[i] = __float_as_uint(own[i % NT]); lo[i] = 0u; }
         } else {
@@ -361,12 +368,12 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
           mbar_wait(&empty_a[sa], ((c / SA) & 1) ^ 1);   // MMAs of chunk c - SA drained stage sa
           fence_after();
         }
-        if (!(a.debug & 4)) {
+        if (!(TC_DEBUG & 4)) {
           tmem_st<NV>(tbase + lane_addr + col + half * NV, hi);
           tmem_st<NV>(tbase + lane_addr + col + ACOLS + half * NV, lo);
         }
       }
-      if (!(a.debug & 4)) tmem_wait_st();
+      if (!(TC_DEBUG & 4)) tmem_wait_st();
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_a[sa]);
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
         mbar_wait_sleep(&empty_a[sb], ((c / SB) & 1) ^ 1);
         const int gc = chunk0 + c;
         if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 0] = clock64();
-        if (a.debug & 8) { mbar_arrive(&full_b[sb]); continue; }
+        if (TC_DEBUG & 8) { mbar_arrive(&full_b[sb]); continue; }
         mbar_expect_tx(&full_b[sb], B_STAGE_BYTES + T_STAGE_BYTES);
         const unsigned char* bsrc = reinterpret_cast<const unsigned char*>(a.b_img) +
                                     ((size_t)group * a.n_chunks_total + gc) * B_STAGE_BYTES;
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
         const uint32_t ahi = tbase + A_COL0 + sa * (2 * ACOLS), alo = ahi + ACOLS;
 #pragma unroll
         for (int t = 0; t < KSTEPS; ++t) {
-          if (a.debug & 2) break;
+          if (TC_DEBUG & 2) break;
           const uint32_t boff = (uint32_t)(2 * t) * LBO;
           const uint32_t acc = (c % SEG != 0 || t > 0) ? 1u : 0u;
           mma_ts<F16>(d_tmem, ahi + COLS_PER_STEP * t, smem_desc(bhi + boff, LBO, SBO), idesc, acc);
@@ -590,10 +597,7 @@ struct TcPlan {
   std::string desc;
 };
 
-static int g_tc_debug = [] {
-  const char* e = getenv("NFS_TC_DEBUG");
-  return e ? atoi(e) : 0;
-}();
+
 
 static long long* g_tc_trace = nullptr;
 extern "C" long long* nfs_tc_trace_enable() {   // profiling hook (not part of the C ABI)
@@ -781,7 +785,6 @@ static cudaError_t launch_main(TcPlan* t, bool fwd, const int* stop, cudaStream_
   a.scale = t->d_scale + (fwd ? 0 : 1);
   a.out = fwd ? t->part_y : t->part_q;
   a.stop = stop;
-  a.debug = g_tc_debug;
   a.trace = g_tc_trace;
   if (a.n_own <= 0) return cudaSuccess;
   void* k = tc_kernel(t->f16, t->nc, t->nt, fwd);

@@ -1,4 +1,7 @@
-"""Time the tensor-core forward kernel alone under NFS_TC_DEBUG modes (set in the env)."""
+"""Per-operator device times of the tensor-core kernels for config B (PREC env = precision).
+
+Profiling switches are compile-time: build a variant with tools/build_variant.sh NAME
+-DNFS_TCI_DEBUG=m (f16x3) and point NFS_B200_LIB at it."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_09233_b200 import _native, simulate
