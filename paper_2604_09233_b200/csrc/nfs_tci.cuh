@@ -13,10 +13,9 @@ TciPlan* tci_create(int64_t K, int64_t L, int G, int nt, int sms, std::string* w
 void tci_destroy(TciPlan* t);
 const char* tci_describe(TciPlan* t);
 const char* tci_last_error();
-// tables on the host: temporal in turns [K][nt], spatial [L][nt] (FP64, zero padded)
-int tci_set_tables(TciPlan* t, const double* tt_turns, const double* rr, cudaStream_t st);
-// same from FP64 device tables [K][nt] / [L][nt] and their per-term max |value| (host arrays);
-// returns 2 when the exact fixed-point phase range is exceeded
+// tables from FP64 device tables (temporal in turns [K][nt], spatial [L][nt], zero padded) and
+// their per-term max |value| (host arrays); returns 2 when the exact fixed-point phase range is
+// exceeded (the caller then uses the FP32 CUDA-core contraction)
 int tci_set_tables_dev(TciPlan* t, const double* d_tt, const double* d_rr, const double* amax_t,
                        const double* amax_r, cudaStream_t st);
 int tci_set_sens(TciPlan* t, const void* d_S, int ldc, cudaStream_t st);
