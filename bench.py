@@ -308,11 +308,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        vals = [cpu_reference_sample(prob)[0] for _ in range(2)]
-        cpu = {"value": float(np.median(vals)), "unit": "applies/s", "cores": _NCPU, "kind": "port",
-               "sample": (f"{CPU_SAMPLE_ROWS} of {K} sample rows (3 reference split blocks of 402 "
-                          "rows) of one E^H E, extrapolated linearly; oracle port of "
-                          "nfs/engine.py:217-223, numpy+OpenBLAS")}
+        # ~10 s of CPU work: three samples of 8 reference split blocks (402 rows each)
+        rows = 8 * 402
+        runs = [cpu_reference_sample(prob, rows=rows) for _ in range(3)]
+        cpu = {"value": float(np.median([v for v, _ in runs])), "unit": "applies/s", "cores": _NCPU,
+               "kind": "port",
+               "sample": (f"3 x {rows} of {K} sample rows (8 reference split blocks of 402 rows) of one "
+                          f"E^H E, {sum(dt for _, dt in runs):.1f} s of CPU work, extrapolated linearly; "
+                          "oracle port of nfs/engine.py:217-223, numpy+OpenBLAS")}
 
     if rank == 0:
         line = {
@@ -320,7 +323,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": {"fp32": "fp32", "fp64": "fp64", "tf32x3": "tf32x3 (fp32 accumulate)",
-                      "f16x3": "f16x3 split (fp32 phase, fp32 accumulate)"}[args.precision],
+                      "f16x3": "f16x3 split contraction (exact int8 phase, fp32 accumulate)"}[args.precision],
             "data": "synthetic (disc phantom, synthetic coils, linear B0; raw data from the device forward model)",
             "config": {"workload": WORKLOAD, "precision": args.precision,
                        "l2": "flushed between steps (256 MiB device write outside the timed events)",
