@@ -38,6 +38,15 @@ inline cudaStream_t alloc_stream() {
 inline cudaError_t dev_alloc(void** p, size_t bytes) {
   cudaStream_t s = alloc_stream();
   cudaError_t e = cudaMallocAsync(p, bytes, s);
+  if (e == cudaErrorMemoryAllocation) {   // give cached pool memory back to the device, retry once
+    cudaGetLastError();
+    int dev = 0;
+    cudaMemPool_t pool;
+    cudaStreamSynchronize(s);
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+      cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(p, bytes, s);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   return e;
 }
