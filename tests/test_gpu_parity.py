@@ -466,3 +466,27 @@ def test_recon_slices_single_rank_matches_recon_full():
     for i, (img, log) in enumerate(out):
         ref, _ = engine.recon_full(slices[i], precision="fp64")
         assert np.array_equal(img.values, ref.values) and len(log.residual_norms) == 6
+
+
+@pytest.mark.parametrize("prec", ["f16x3", "tf32x3", "fp32"])
+@pytest.mark.parametrize("K,L,G,P1", [(1, 1, 1, 1), (7, 5, 2, 2), (130, 40, 9, 4), (257, 97, 17, 9),
+                                      (64, 600, 33, 12), (500, 65, 64, 20), (31, 1025, 5, 17)])
+def test_fast_modes_edge_shapes(prec, K, L, G, P1):
+    """Ragged owner tiles / chunks, every coil-group width (NC 8/16/32, several groups), term
+    counts that pad the int8 phase K (ntp = roundup(P+1, 8)), single sample / voxel: the fast
+    modes agree with the FP64 device path (itself pinned to the oracle) within 2e-5."""
+    rng = np.random.default_rng(K * 131 + L * 7 + G)
+    spatial = rng.standard_normal((P1, L)) * 0.6
+    temporal = rng.standard_normal((K, P1)) * 2.5
+    sens = rng.standard_normal((L, G)) + 1j * rng.standard_normal((L, G))
+    p = rng.standard_normal(L) + 1j * rng.standard_normal(L)
+    sig = rng.standard_normal((K, G)) + 1j * rng.standard_normal((K, G))
+    out = {}
+    for mode in ("fp64", prec):
+        plan = Plan(K, L, G, P1, mode)
+        plan.set_tables(temporal, spatial)
+        plan.set_sens(sens)
+        out[mode] = (plan.apply_E(p), plan.apply_EH(sig), plan.apply_EHE(p))
+        plan.close()
+    for a, b in zip(out[prec], out["fp64"]):
+        assert rel(a, b) < 2e-5
