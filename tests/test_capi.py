@@ -122,3 +122,24 @@ def test_choose_block_starts_and_sharding():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             sizes = [b - a for a, b in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """The ABI is usable from plain C (what a cgo / JNI / N-API shim would compile against):
+    the header compiles as C99 and a C program links against the built library (no GPU calls;
+    it only queries the version string)."""
+    import shutil
+    import subprocess
+    from paper_2604_09233_b200 import build
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    lib_path = build.build()
+    src = tmp_path / "abi.c"
+    src.write_text('#include <stdio.h>\n#include "nfs_b200.h"\n'
+                   "int main(void) { nfs_plan* p = 0; (void)p; puts(nfs_version()); return 0; }\n")
+    exe = tmp_path / "abi"
+    subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src),
+                    lib_path, "-o", str(exe), f"-Wl,-rpath,{os.path.dirname(lib_path)}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert out.strip()
