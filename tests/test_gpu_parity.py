@@ -172,6 +172,26 @@ def test_config_a_fast_mode_tolerance(prec):
     assert np.allclose(log.residual_norms[:10], g["res"][:10], rtol=1e-3)
 
 
+@pytest.mark.parametrize("prec", ["fp32", "tf32x3", "f16x3"])
+def test_config_a_masked_fast_mode_tolerance(prec):
+    """Masked config A (phantom support, intensity correction, k-filter) in the fast modes: the
+    FP32-class operators track the reference to ~2e-6 at iteration 5; the CG amplifies
+    per-apply rounding from iteration ~6 on (the masked system is CG-chaotic even in FP64), so
+    iteration 10 is pinned at 1e-4 (measured: fp32 4e-6, tf32x3 3e-5, f16x3 3.6e-5 -- the
+    tensor-core accumulation truncates between drains, nfs_tci.cu) and the image at 1e-2."""
+    g = golden("config_a")
+    pm = simulate.make_problem("A_mask")
+    seen = {}
+    img, log = engine.recon_full(inputs_from(pm.grid, g["sigma"], pm.spatial, pm.temporal, pm.sens,
+                                             20, mask=pm.mask_r, intensity=pm.intensity,
+                                             kfilter=g["kfilter"]),
+                                 callback=lambda n, r: seen.__setitem__(n, r), precision=prec)
+    assert rel(seen[5], g["rho_iters_mask"][0]) < 5e-6
+    assert rel(seen[10], g["rho_iters_mask"][1]) < 1e-4
+    assert rel(img.values, g["values_mask"]) < 1e-2
+    assert np.allclose(log.residual_norms[:5], g["res_mask"][:5], rtol=1e-4)
+
+
 def test_config_a_masked_with_filter_fp64():
     """Masked config A is CG-chaotic after ~12 iterations even in FP64: the reference's own
     split-vs-full variants drift apart 1e-14 -> 2.5e-7 between iterations 11 and 19.  So the
