@@ -65,6 +65,10 @@ int nfs_plan_attach_comm(nfs_plan* plan, const void* nccl_unique_id, int32_t ran
 
 /* Basis tables: temporal rows of this rank (K x P1) and spatial (P1 x L_R). */
 int nfs_set_tables(nfs_plan* plan, const double* temporal, const double* spatial);
+/* Same, with the spatial table voxel-major (L_R x P1): the memory of the Fortran-ordered
+ * (P1, L_R) array that np.vstack([b0, harm.T]) in build_bases (nfs/engine.py:252-280)
+ * returns, so the caller uploads it as is instead of transposing on the host. */
+int nfs_set_tables_t(nfs_plan* plan, const double* temporal, const double* spatial_t);
 /* Same, with the spatial table evaluated ON THE DEVICE from the masked voxels' linear grid
  * indices (ix + nx (iy + ny iz)), their B0 (rad/s), the grid extents dims[3], FOV fov[3] (m)
  * and the harmonic order 1..3 -- replaces engine.build_bases (nfs/engine.py:252-280) +

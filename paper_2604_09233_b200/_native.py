@@ -37,6 +37,7 @@ SIGNATURES = {
     "nfs_plan_set_stream": (_c_i32, [_c_void_p, _c_void_p]),
     "nfs_plan_attach_comm": (_c_i32, [_c_void_p, ctypes.c_char_p, _c_i32, _c_i32]),
     "nfs_set_tables": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
+    "nfs_set_tables_t": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
     "nfs_set_tables_grid": (_c_i32, [_c_void_p, _c_dbl_p, ctypes.POINTER(_c_i64), _c_dbl_p,
                                      ctypes.POINTER(_c_i32), _c_dbl_p, _c_i32]),
     "nfs_set_sens": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
@@ -147,6 +148,12 @@ class Plan:
     def set_tables(self, temporal, spatial):
         k, l, _, p1 = self.shape
         t = np.ascontiguousarray(temporal, dtype=np.float64).reshape(k, p1)
+        spatial = np.asarray(spatial)
+        if (spatial.dtype == np.float64 and spatial.shape == (p1, l) and spatial.flags.f_contiguous
+                and not spatial.flags.c_contiguous):
+            # build_bases' vstack yields a Fortran-ordered table: upload it voxel-major as is
+            _check(self._lib.nfs_set_tables_t(self._h, _dp(t), _dp(spatial.T)))
+            return
         s = np.ascontiguousarray(spatial, dtype=np.float64).reshape(p1, l)
         _check(self._lib.nfs_set_tables(self._h, _dp(t), _dp(s)))
 

@@ -10,7 +10,8 @@ cudaError_t launch_spatial_from_grid(const int64_t* d_vox, const double* d_b0, i
 cudaError_t launch_col_absmax(const double* d_tab, int64_t n, int nt, unsigned long long* d_out, cudaStream_t st);
 cudaError_t launch_to_float(const double* d_in, float* d_out, int64_t n, cudaStream_t st);
 cudaError_t launch_prep_tables(const double* d_temporal, const double* d_spatial, int64_t K, int64_t L, int p1,
-                               int nt, double* d_tt, double* d_rr, cudaStream_t st);
+                               int nt, double* d_tt, double* d_rr, cudaStream_t st,
+                               bool spatial_lp = false);
 cudaError_t launch_prep_sens(const double2* d_sens, const double* d_j, int64_t L, int g, int ldc, bool fp64,
                              void* d_out, cudaStream_t st);
 cudaError_t launch_count_nonfinite(const double* d_x, int64_t n, unsigned int* d_out, cudaStream_t st);

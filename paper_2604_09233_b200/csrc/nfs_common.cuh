@@ -57,6 +57,10 @@ inline void dev_free(void* p) {
 }
 
 
+// Host -> device copy of a caller (pageable) array through a pinned staging ring with
+// multi-threaded staging (nfs_upload.cu); same semantics as cudaMemcpyAsync from pageable memory.
+cudaError_t h2d(void* dst, const void* src, size_t bytes, cudaStream_t st);
+
 template <typename T> struct C2;
 template <> struct C2<float> { using type = float2; };
 template <> struct C2<double> { using type = double2; };

@@ -380,7 +380,8 @@ struct DevScratch {
   }
 };
 
-extern "C" int nfs_set_tables(nfs_plan* P, const double* temporal, const double* spatial) {
+// spatial_lp: the spatial table is voxel-major [L][P1] (nfs_set_tables_t) instead of [P1][L]
+static int set_tables_impl(nfs_plan* P, const double* temporal, const double* spatial, bool spatial_lp) {
   if (!P || (!temporal && P->K > 0) || !spatial) return fail(NFS_ERR_INVALID, "null table");
   NFS_CUDA(cudaSetDevice(P->device));
   const int nt = P->NT, p1 = P->P1;
@@ -392,10 +393,18 @@ extern "C" int nfs_set_tables(nfs_plan* P, const double* temporal, const double*
   NFS_CUDA(sc.get(&d_spat, (size_t)p1 * L * 8));
   NFS_CUDA(sc.get(&d_tt, (size_t)K * nt * 8));
   NFS_CUDA(sc.get(&d_rr, (size_t)L * nt * 8));
-  if (K > 0) NFS_CUDA(cudaMemcpyAsync(d_temp, temporal, (size_t)K * p1 * 8, cudaMemcpyHostToDevice, P->stream));
-  NFS_CUDA(cudaMemcpyAsync(d_spat, spatial, (size_t)p1 * L * 8, cudaMemcpyHostToDevice, P->stream));
-  NFS_CUDA(nfs::launch_prep_tables(d_temp, d_spat, K, L, p1, nt, d_tt, d_rr, P->stream));
+  if (K > 0) NFS_CUDA(nfs::h2d(d_temp, temporal, (size_t)K * p1 * 8, P->stream));
+  NFS_CUDA(nfs::h2d(d_spat, spatial, (size_t)p1 * L * 8, P->stream));
+  NFS_CUDA(nfs::launch_prep_tables(d_temp, d_spat, K, L, p1, nt, d_tt, d_rr, P->stream, spatial_lp));
   return finish_tables(P, d_tt, d_rr);
+}
+
+extern "C" int nfs_set_tables(nfs_plan* P, const double* temporal, const double* spatial) {
+  return set_tables_impl(P, temporal, spatial, false);
+}
+
+extern "C" int nfs_set_tables_t(nfs_plan* P, const double* temporal, const double* spatial_t) {
+  return set_tables_impl(P, temporal, spatial_t, true);
 }
 
 // Spatial table evaluated on the device from the masked voxel indices: same
@@ -428,7 +437,7 @@ extern "C" int nfs_set_tables_grid(nfs_plan* P, const double* temporal, const in
   NFS_CUDA(sc.get(&d_rr, (size_t)L * nt * 8));
   NFS_CUDA(cudaMemcpyAsync(d_vox, vox_index, L * 8, cudaMemcpyHostToDevice, P->stream));
   NFS_CUDA(cudaMemcpyAsync(d_b0, b0_masked, L * 8, cudaMemcpyHostToDevice, P->stream));
-  if (K > 0) NFS_CUDA(cudaMemcpyAsync(d_temp, temporal, (size_t)K * p1 * 8, cudaMemcpyHostToDevice, P->stream));
+  if (K > 0) NFS_CUDA(nfs::h2d(d_temp, temporal, (size_t)K * p1 * 8, P->stream));
   NFS_CUDA(nfs::launch_prep_tables(d_temp, nullptr, K, 0, p1, nt, d_tt, nullptr, P->stream));
   NFS_CUDA(nfs::launch_spatial_from_grid(d_vox, d_b0, L, nt, dims, fov, order, d_rr, P->stream));
   return finish_tables(P, d_tt, d_rr);
@@ -442,7 +451,7 @@ extern "C" int nfs_set_sens(nfs_plan* P, const double* sens, const double* inten
   double2* d_sens = nullptr;
   double* d_j = nullptr;
   NFS_CUDA(sc.get(&d_sens, (size_t)L * P->G * sizeof(double2)));
-  NFS_CUDA(cudaMemcpyAsync(d_sens, sens, (size_t)L * P->G * sizeof(double2), cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(nfs::h2d(d_sens, sens, (size_t)L * P->G * sizeof(double2), P->stream));
   if (intensity) {
     NFS_CUDA(sc.get(&d_j, (size_t)L * 8));
     NFS_CUDA(cudaMemcpyAsync(d_j, intensity, (size_t)L * 8, cudaMemcpyHostToDevice, P->stream));
@@ -464,7 +473,7 @@ extern "C" int nfs_set_sens(nfs_plan* P, const double* sens, const double* inten
 static int upload_samples(nfs_plan* P, const double* sigma, void* dst) {
   const size_t n = (size_t)P->K * P->G;
   NFS_TRY(ensure_io(P, std::max<size_t>(n, (size_t)P->L)));
-  NFS_CUDA(cudaMemcpyAsync(P->d_io, sigma, n * sizeof(double2), cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(nfs::h2d(P->d_io, sigma, n * sizeof(double2), P->stream));
   NFS_CUDA(nfs::launch_pack(P->prec == NFS_PREC_FP64 ? 1 : 0, P->d_io, dst, P->K, P->G, P->ldc, P->stream));
   return NFS_OK;
 }
@@ -474,7 +483,7 @@ extern "C" int nfs_set_samples(nfs_plan* P, const double* sigma) {
   NFS_CUDA(cudaSetDevice(P->device));
   const size_t n = (size_t)P->K * P->G;
   NFS_TRY(ensure_io(P, std::max<size_t>(n, (size_t)P->L)));
-  NFS_CUDA(cudaMemcpyAsync(P->d_io, sigma, n * sizeof(double2), cudaMemcpyHostToDevice, P->stream));
+  NFS_CUDA(nfs::h2d(P->d_io, sigma, n * sizeof(double2), P->stream));
   unsigned int bad = 0;
   unsigned int* d_bad = reinterpret_cast<unsigned int*>(P->d_partials);   // reduction scratch
   NFS_CUDA(nfs::launch_count_nonfinite(reinterpret_cast<const double*>(P->d_io), (int64_t)n * 2, d_bad, P->stream));

@@ -334,6 +334,28 @@ def test_config_d_device_synthesis_rows(problem_d, prec, tol):
     plan.close()
 
 
+@pytest.mark.parametrize("prec", ["fp64", "f16x3"])
+def test_spatial_table_layouts_identical(prec, rng):
+    """A Fortran-ordered spatial table (what build_bases' vstack returns) goes up voxel-major
+    through nfs_set_tables_t without a host transpose; the operators are bit-identical to the
+    C-ordered upload through nfs_set_tables."""
+    K, L, G, P1 = 700, 333, 5, 4
+    spatial_c = np.ascontiguousarray(rng.standard_normal((P1, L)))
+    spatial_f = np.asfortranarray(spatial_c)
+    assert spatial_f.flags.f_contiguous and not spatial_f.flags.c_contiguous
+    temporal = rng.standard_normal((K, P1))
+    sens = rng.standard_normal((L, G)) + 1j * rng.standard_normal((L, G))
+    p = rng.standard_normal(L) + 1j * rng.standard_normal(L)
+    out = []
+    for sp in (spatial_c, spatial_f):
+        plan = Plan(K, L, G, P1, prec)
+        plan.set_tables(temporal, sp)
+        plan.set_sens(sens)
+        out.append(plan.apply_EHE(p))
+        plan.close()
+    assert np.array_equal(out[0], out[1])
+
+
 def test_f16x3_phase_range_fallback():
     """A basis whose phase exceeds the exact int8 fixed-point range (|t'_p r_p| > 2^12 turns)
     runs the f16x3 plan on the FP32 CUDA-core contraction (said so in describe()), agreeing

@@ -6,8 +6,8 @@ cd "$(dirname "$0")/.."
 python -m paper_2604_09233_b200.build >/dev/null
 name=$1; shift
 mkdir -p tools/variants build/variants
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -O3 -Iinclude "$@" \
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp -Xptxas -O3 -Iinclude "$@" \
   -Ipaper_2604_09233_b200/csrc -c ${TCI_SRC:-paper_2604_09233_b200/csrc/nfs_tci.cu} -o build/variants/nfs_tci_$name.o
 objs=$(ls build/nfs_b200/*.o | grep -v nfs_tci.o)
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o tools/variants/lib_$name.so $objs build/variants/nfs_tci_$name.o -ldl
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o tools/variants/lib_$name.so $objs build/variants/nfs_tci_$name.o -ldl -lgomp
 echo tools/variants/lib_$name.so
