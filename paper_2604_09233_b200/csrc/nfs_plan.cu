@@ -249,6 +249,7 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
     return bail(s);
   if (P->split_f > 1 && (s = alloc(&P->d_party, (size_t)P->split_f * K * P->ldc * t2)))
     return bail(s);
+  std::string tci_note;
   if (precision == NFS_PREC_TF32X3) {
     std::string why;
     P->tc = nfs::tc_create(P->K, P->L, P->G, nt, sms, false, &why);
@@ -256,7 +257,10 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
   } else if (precision == NFS_PREC_F16X3) {
     std::string why;
     P->tci = nfs::tci_create(P->K, P->L, P->G, nt, sms, &why);
-    if (!P->tci) return bail(fail(NFS_ERR_INVALID, "tensor-core path unavailable: " + why));
+    // too many basis terms for the kernel's shared-memory staging: run the plan on the FP32
+    // CUDA-core contraction (as for a phase range the exact int8 phase cannot hold) and say so
+    if (!P->tci && why.rfind("shared memory budget", 0) == 0) tci_note = " [f16x3 unavailable for " + std::to_string(P->P1) + " basis terms (" + why + "): FP32 CUDA-core contraction]";
+    else if (!P->tci) return bail(fail(NFS_ERR_INVALID, "tensor-core path unavailable: " + why));
   }
   char buf[512];
   snprintf(buf, sizeof buf,
@@ -266,6 +270,7 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
            (long long)P->K, (long long)P->L, P->G, P->P1, nt, P->NC, P->NG, P->split_f, occ_f,
            own_f, P->split_a, occ_a, own_a, P->tc ? nfs::tc_describe(P->tc) : (P->tci ? nfs::tci_describe(P->tci) : ""));
   P->desc = buf;
+  P->desc += tci_note;
   if (cudaStreamSynchronize(P->stream) != cudaSuccess)
     return bail(fail(NFS_ERR_CUDA, "plan init failed"));
   *out = P;

@@ -378,6 +378,29 @@ def test_f16x3_phase_range_fallback():
     assert rel(out["f16x3"], out["fp32"]) < 1e-5
 
 
+@pytest.mark.parametrize("G", [8, 32])
+def test_f16x3_many_terms(G):
+    """P+1 = 30 basis terms: with 8 coils the f16x3 kernel's shared-memory staging still fits;
+    with 32 it does not and the plan runs on the FP32 CUDA-core contraction, saying so in
+    describe().  Either way the result agrees with fp32."""
+    rng = np.random.default_rng(12)
+    L, K, P1 = 300, 400, 30
+    spatial = rng.standard_normal((P1, L)) * 0.3
+    temporal = rng.standard_normal((K, P1))
+    sens = rng.standard_normal((L, G)) + 1j * rng.standard_normal((L, G))
+    p = rng.standard_normal(L) + 1j * rng.standard_normal(L)
+    out = {}
+    for prec in ("f16x3", "fp32"):
+        plan = Plan(K, L, G, P1, prec)
+        plan.set_tables(temporal, spatial)
+        plan.set_sens(sens)
+        out[prec] = plan.apply_EHE(p)
+        if prec == "f16x3":
+            assert ("FP32 CUDA-core contraction" in plan.describe()) == (G == 32)
+        plan.close()
+    assert rel(out["f16x3"], out["fp32"]) < 1e-5
+
+
 @pytest.mark.parametrize("prec", ["fp64", "fp32", "f16x3", "tf32x3"])
 def test_device_bases_bitwise(prec):
     """the spatial table evaluated on the GPU (nfs_set_tables_grid) is bit-identical
