@@ -74,7 +74,12 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.rows.append((time.perf_counter(), parts))
+
+    def window(self, t0, t1):
+        """Keep the samples taken inside [t0, t1] (the timed region; nvidia-smi was started
+        before the warm-up so it is sampling by then)."""
+        self.t0, self.t1 = t0, t1
 
     def __exit__(self, *exc):
         if self.proc:
@@ -85,14 +90,19 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        rows = [r for t, r in self.rows if t0 is None or t0 <= t <= t1]
+        if not rows:   # region shorter than one sampling period: nearest samples
+            rows = [r for _, r in sorted(self.rows, key=lambda tr: abs(tr[0] - (t0 or 0)))[:3]]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        self_rows = rows
+        sm = [float(r[0]) for r in self_rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self_rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:]) if v.strip().lower() == "active"})
+        reasons = sorted({n for r in self_rows for n, v in zip(names, r[3:]) if v.strip().lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self_rows)}
 
 
 # ------------------------------------------------------------------ CPU legs
@@ -150,7 +160,7 @@ def run_reference_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default=os.environ.get("NFS_BENCH_PRECISION", "f16x3"),
@@ -194,6 +204,10 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     launches = plan.launches_per_apply()
 
+    clk = ClockSampler(local).__enter__()   # sampling from before the warm-up
+    t_wait = time.perf_counter()
+    while not clk.rows and time.perf_counter() - t_wait < 3.0 and clk.proc is not None:
+        time.sleep(0.01)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             plan.apply_EHE_resident(1)
@@ -203,16 +217,18 @@ def main():
         torch.cuda.synchronize()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
-        with ClockSampler(local) as clk:
-            for i in range(args.steps):
-                flush.fill_(float(i))            # evict L2 between steps (outside the events)
-                ev[i][0].record(stream)
-                plan.apply_EHE_resident(1)
-                ev[i][1].record(stream)
-            stream.synchronize()
+        t_start = time.perf_counter()
+        for i in range(args.steps):
+            flush.fill_(float(i))            # evict L2 between steps (outside the events)
+            ev[i][0].record(stream)
+            plan.apply_EHE_resident(1)
+            ev[i][1].record(stream)
+        stream.synchronize()
         torch.cuda.synchronize()
+        clk.window(t_start, time.perf_counter())
         if world > 1:
             dist.barrier()
+    clk.__exit__(None, None, None)
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
     if world > 1:
         t = torch.tensor([total_ms], device="cuda")
