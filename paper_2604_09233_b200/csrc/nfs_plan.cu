@@ -175,6 +175,8 @@ static int ensure_io(nfs_plan* P, size_t n_c128) {
 extern "C" const char* nfs_last_error(void) { return g_err.c_str(); }
 extern "C" const char* nfs_version(void) { return "nfs_b200 0.1 (sm_100a)"; }
 
+static int f16x3_fallback(nfs_plan* P, const std::string& reason);
+
 extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxels,
                                int32_t n_coils, int32_t n_terms, int32_t precision,
                                int32_t device) {
@@ -257,9 +259,9 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
   } else if (precision == NFS_PREC_F16X3) {
     std::string why;
     P->tci = nfs::tci_create(P->K, P->L, P->G, nt, sms, &why);
-    // too many basis terms for the kernel's shared-memory staging: run the plan on the FP32
-    // CUDA-core contraction (as for a phase range the exact int8 phase cannot hold) and say so
-    if (!P->tci && why.rfind("shared memory budget", 0) == 0) tci_note = " [f16x3 unavailable for " + std::to_string(P->P1) + " basis terms (" + why + "): FP32 CUDA-core contraction]";
+    // too many basis terms for the kernel's shared-memory staging: fall back (after the
+    // description is written, below)
+    if (!P->tci && why.rfind("shared memory budget", 0) == 0) tci_note = std::to_string(P->P1) + " basis terms";
     else if (!P->tci) return bail(fail(NFS_ERR_INVALID, "tensor-core path unavailable: " + why));
   }
   char buf[512];
@@ -270,7 +272,10 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
            (long long)P->K, (long long)P->L, P->G, P->P1, nt, P->NC, P->NG, P->split_f, occ_f,
            own_f, P->split_a, occ_a, own_a, P->tc ? nfs::tc_describe(P->tc) : (P->tci ? nfs::tci_describe(P->tci) : ""));
   P->desc = buf;
-  P->desc += tci_note;
+  if (!tci_note.empty()) {
+    const int s = f16x3_fallback(P, tci_note);
+    if (s) return bail(s);
+  }
   if (cudaStreamSynchronize(P->stream) != cudaSuccess)
     return bail(fail(NFS_ERR_CUDA, "plan init failed"));
   *out = P;
@@ -324,6 +329,27 @@ extern "C" int nfs_plan_attach_comm(nfs_plan* P, const void* uid, int32_t rank, 
 }
 
 // ------------------------------------------------------------------ inputs
+// An f16x3 plan whose basis the exact int8 phase kernel cannot take (phase range, or more terms
+// than its shared-memory staging holds) runs on the TF32x3 tensor-core contraction (FP32 phase,
+// the same accuracy class), else on the FP32 CUDA-core contraction; the description says which.
+static int f16x3_fallback(nfs_plan* P, const std::string& reason) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device);
+  std::string why;
+  P->tc = nfs::tc_create(P->K, P->L, P->G, P->NT, sms, false, &why);
+  if (!P->tc) {
+    P->desc += " [f16x3 unavailable for " + reason + ": FP32 CUDA-core contraction]";
+    return NFS_OK;
+  }
+  if (P->have_sens && nfs::tc_set_sens(P->tc, P->d_S, P->ldc, P->stream))
+    return fail(NFS_ERR_CUDA, "tc sens: " + std::string(nfs::tc_last_error()));
+  if (P->have_tables && nfs::tc_set_tables(P->tc, P->d_T, P->d_R, P->stream))
+    return fail(NFS_ERR_CUDA, "tc tables: " + std::string(nfs::tc_last_error()));
+  P->desc += " [f16x3 unavailable for " + reason + ": TF32x3 tensor-core contraction" +
+             nfs::tc_describe(P->tc) + "]";
+  return NFS_OK;
+}
+
 // FP64 device tables tt [K][nt] (turns) and rr [L][nt] -> the plan's operator tables, the
 // tensor-core images, and the int8-phase fixed-point scales (all on the device)
 static int finish_tables(nfs_plan* P, const double* d_tt, const double* d_rr) {
@@ -356,12 +382,10 @@ static int finish_tables(nfs_plan* P, const double* d_tt, const double* d_rr) {
     for (int p = 0; p < 2 * nt; ++p) memcpy(&amax[p], &mx[p], 8);
     int st = nfs::tci_set_tables_dev(P->tci, d_tt, d_rr, amax.data(), amax.data() + nt, P->stream);
     if (st == 2) {
-      // the exact int8 phase cannot represent this basis (some |t'_p r_p| > 2^12 turns): run
-      // the plan on the FP32 CUDA-core contraction instead (same buffers, same results within
-      // the FP32 tolerance) and say so in the description
+      // the exact int8 phase cannot represent this basis (some |t'_p r_p| > 2^12 turns)
       nfs::tci_destroy(P->tci);
       P->tci = nullptr;
-      P->desc += " [f16x3 unavailable for this basis (phase range): FP32 CUDA-core contraction]";
+      NFS_TRY(f16x3_fallback(P, "this basis (phase range)"));
     } else if (st) {
       return fail(NFS_ERR_INVALID, "tci tables: " + std::string(nfs::tci_last_error()));
     }

@@ -358,8 +358,8 @@ def test_spatial_table_layouts_identical(prec, rng):
 
 def test_f16x3_phase_range_fallback():
     """A basis whose phase exceeds the exact int8 fixed-point range (|t'_p r_p| > 2^12 turns)
-    runs the f16x3 plan on the FP32 CUDA-core contraction (said so in describe()), agreeing
-    with an fp32 plan."""
+    runs the f16x3 plan on the TF32x3 tensor-core contraction (FP32 phase; said so in
+    describe()), agreeing with an fp32 plan."""
     rng = np.random.default_rng(11)
     L, K, G, P1 = 200, 300, 8, 3
     spatial = rng.standard_normal((P1, L))
@@ -373,7 +373,7 @@ def test_f16x3_phase_range_fallback():
         plan.set_sens(sens)
         out[prec] = plan.apply_EHE(p)
         if prec == "f16x3":
-            assert "FP32 CUDA-core contraction" in plan.describe()
+            assert "f16x3 unavailable" in plan.describe() and "TF32x3 tensor-core contraction" in plan.describe()
         plan.close()
     assert rel(out["f16x3"], out["fp32"]) < 1e-5
 
@@ -381,7 +381,7 @@ def test_f16x3_phase_range_fallback():
 @pytest.mark.parametrize("G", [8, 32])
 def test_f16x3_many_terms(G):
     """P+1 = 30 basis terms: with 8 coils the f16x3 kernel's shared-memory staging still fits;
-    with 32 it does not and the plan runs on the FP32 CUDA-core contraction, saying so in
+    with 32 it does not and the plan runs on the TF32x3 tensor-core contraction, saying so in
     describe().  Either way the result agrees with fp32."""
     rng = np.random.default_rng(12)
     L, K, P1 = 300, 400, 30
@@ -396,7 +396,7 @@ def test_f16x3_many_terms(G):
         plan.set_sens(sens)
         out[prec] = plan.apply_EHE(p)
         if prec == "f16x3":
-            assert ("FP32 CUDA-core contraction" in plan.describe()) == (G == 32)
+            assert ("TF32x3 tensor-core contraction" in plan.describe()) == (G == 32)
         plan.close()
     assert rel(out["f16x3"], out["fp32"]) < 1e-5
 
