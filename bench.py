@@ -205,30 +205,32 @@ def main():
     launches = plan.launches_per_apply()
 
     clk = ClockSampler(local).__enter__()   # sampling from before the warm-up
-    t_wait = time.perf_counter()
-    while not clk.rows and time.perf_counter() - t_wait < 3.0 and clk.proc is not None:
-        time.sleep(0.01)
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            plan.apply_EHE_resident(1)
-        stream.synchronize()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)]
-        t_start = time.perf_counter()
-        for i in range(args.steps):
-            flush.fill_(float(i))            # evict L2 between steps (outside the events)
-            ev[i][0].record(stream)
-            plan.apply_EHE_resident(1)
-            ev[i][1].record(stream)
-        stream.synchronize()
-        torch.cuda.synchronize()
-        clk.window(t_start, time.perf_counter())
-        if world > 1:
-            dist.barrier()
-    clk.__exit__(None, None, None)
+    try:
+        t_wait = time.perf_counter()
+        while not clk.rows and time.perf_counter() - t_wait < 3.0 and clk.proc is not None:
+            time.sleep(0.01)
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                plan.apply_EHE_resident(1)
+            stream.synchronize()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)]
+            t_start = time.perf_counter()
+            for i in range(args.steps):
+                flush.fill_(float(i))            # evict L2 between steps (outside the events)
+                ev[i][0].record(stream)
+                plan.apply_EHE_resident(1)
+                ev[i][1].record(stream)
+            stream.synchronize()
+            torch.cuda.synchronize()
+            clk.window(t_start, time.perf_counter())
+            if world > 1:
+                dist.barrier()
+    finally:
+        clk.__exit__(None, None, None)
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
     if world > 1:
         t = torch.tensor([total_ms], device="cuda")
