@@ -380,9 +380,8 @@ def test_f16x3_phase_range_fallback():
 
 @pytest.mark.parametrize("G", [8, 32])
 def test_f16x3_many_terms(G):
-    """P+1 = 30 basis terms: with 8 coils the f16x3 kernel's shared-memory staging still fits;
-    with 32 it does not and the plan runs on the TF32x3 tensor-core contraction, saying so in
-    describe().  Either way the result agrees with fp32."""
+    """P+1 = 30 basis terms (the plan maximum is 32): the f16x3 kernel's shared-memory staging
+    holds them at 8 and at 32 coils (no fallback), and the result agrees with fp32."""
     rng = np.random.default_rng(12)
     L, K, P1 = 300, 400, 30
     spatial = rng.standard_normal((P1, L)) * 0.3
@@ -396,7 +395,7 @@ def test_f16x3_many_terms(G):
         plan.set_sens(sens)
         out[prec] = plan.apply_EHE(p)
         if prec == "f16x3":
-            assert ("TF32x3 tensor-core contraction" in plan.describe()) == (G == 32)
+            assert "unavailable" not in plan.describe() and "int8 phase" in plan.describe()
         plan.close()
     assert rel(out["f16x3"], out["fp32"]) < 1e-5
 
