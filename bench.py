@@ -284,6 +284,10 @@ def main():
     if args.precision != "fp64":
         mufu_peak = 148 * 16 * 1.965e9
         roofline["mufu_frac"] = 2.0 * float(k_loc) * L / (dom_ms * 1e-3) / mufu_peak
+        # the highest `frac` this algorithm can reach: the phasor's 2 MUFU ops per pair at the
+        # SFU peak bound the time per launch from below, whatever the tensor cores do
+        t_floor = 2.0 * float(k_loc) * L / mufu_peak
+        roofline["frac_ceiling_mufu"] = flops_1 / t_floor / 1e12 / peak
     if args.precision in ("f16x3", "tf32x3"):
         # the split MMA executes 3 products on the real-ified operands: 3 x 2 x (2 x 2G) per pair
         executed = float(k_loc) * L * 3 * 2 * 2 * (2 * G) * 2 / 2
