@@ -43,7 +43,7 @@ extern "C" {
 #define NFS_PREC_FP32 0   /* FP32 phase + MUFU sincos + FP32 FMA contraction (fast mode)  */
 #define NFS_PREC_FP64 1   /* FP64 phase, FP64 sincospi, FP64 FMA (parity mode)            */
 #define NFS_PREC_TF32X3 2 /* tcgen05 3xTF32 split contraction, FP32 phase (tensor mode)   */
-#define NFS_PREC_F16X3 3  /* tcgen05 3xFP16 split contraction (scaled B), FP32 phase        */
+#define NFS_PREC_F16X3 3  /* tcgen05 3xFP16 split contraction (scaled B), exact int8 tcgen05 phase */
 
 typedef struct nfs_plan nfs_plan;
 
