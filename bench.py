@@ -288,6 +288,8 @@ def main():
         # SFU peak bound the time per launch from below, whatever the tensor cores do
         t_floor = 2.0 * float(k_loc) * L / mufu_peak
         roofline["frac_ceiling_mufu"] = flops_1 / t_floor / 1e12 / peak
+        if clocks.get("sm_mhz"):   # against the SFU peak at the clock the run actually had
+            roofline["mufu_frac_at_observed_clock"] = roofline["mufu_frac"] * 1965.0 / clocks["sm_mhz"]
     if args.precision in ("f16x3", "tf32x3"):
         # the split MMA executes 3 products on the real-ified operands: 3 x 2 x (2 x 2G) per pair
         executed = float(k_loc) * L * 3 * 2 * 2 * (2 * G) * 2 / 2
