@@ -18,6 +18,7 @@
  * Status codes map onto the reference's exception classes:
  *   NFS_ERR_INVALID / NFS_ERR_NONFINITE / NFS_ERR_BREAKDOWN / NFS_ERR_NONFINITE_ITERATE
  *     -> EngineError        (nfs/engine.py:22, raised at :49-69, :139-140, :164-165, :173-174)
+ *   NFS_ERR_ABORTED (the iteration callback returned non-zero) -> the callback's own exception
  *   NFS_ERR_BUDGET -> MemoryBudgetError (nfs/engine.py:26, :132-137)
  * nfs_last_error() returns the thread-local message of the last failing call.
  */
@@ -38,6 +39,7 @@ extern "C" {
 #define NFS_ERR_CUDA 5
 #define NFS_ERR_NCCL 6
 #define NFS_ERR_NONFINITE_ITERATE 7
+#define NFS_ERR_ABORTED 8
 
 /* operator arithmetic */
 #define NFS_PREC_FP32 0   /* FP32 phase + MUFU sincos + FP32 FMA contraction (fast mode)  */
@@ -48,8 +50,10 @@ extern "C" {
 typedef struct nfs_plan nfs_plan;
 
 /* Called once per CG iteration when registered: n (1-based) and the restricted iterate
- * (host copy, complex128, L_R entries).  Mirrors `callback(n, rho)` of nfs/engine.py:177. */
-typedef void (*nfs_iter_callback)(int32_t n, const double* rho, void* user);
+ * (host copy, complex128, L_R entries).  Mirrors `callback(n, rho)` of nfs/engine.py:177.
+ * A non-zero return aborts the solve right there (the reference's CG stops at a callback that
+ * raises): nfs_cg_solve returns NFS_ERR_ABORTED with *n_done = n. */
+typedef int32_t (*nfs_iter_callback)(int32_t n, const double* rho, void* user);
 
 /* Plan for one device.  n_samples = rows held by THIS rank (sample sharding).
  * Replaces the implicit state of recon_full/recon_split (nfs/engine.py:125,182). */

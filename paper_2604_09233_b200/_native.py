@@ -24,11 +24,12 @@ NFS_ERR_BUDGET = 4
 NFS_ERR_CUDA = 5
 NFS_ERR_NCCL = 6
 NFS_ERR_NONFINITE_ITERATE = 7
+NFS_ERR_ABORTED = 8
 
 PRECISIONS = {"fp32": 0, "fp64": 1, "tf32x3": 2, "f16x3": 3}
 
 _c_i32, _c_i64, _c_dbl_p, _c_void_p = ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p
-CALLBACK = ctypes.CFUNCTYPE(None, ctypes.c_int32, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p)
+CALLBACK = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p)
 
 # name -> (restype, argtypes); must match include/nfs_b200.h exactly
 SIGNATURES = {
@@ -222,8 +223,10 @@ class Plan:
             try:
                 arr = np.ctypeslib.as_array(ptr, shape=(2 * l,)).view(np.complex128).copy()
                 callback(int(n), arr)
-            except BaseException as exc:  # propagate after the C call returns
+                return 0
+            except BaseException as exc:  # abort the solve here, re-raise after the C call returns
                 err.append(exc)
+                return 1
 
         cfun = CALLBACK(_cb) if callback is not None else CALLBACK()
         status = self._lib.nfs_cg_solve(self._h, int(n_iter), cfun, None, _dp(rho.view(np.float64)),

@@ -819,7 +819,7 @@ extern "C" int nfs_cg_solve(nfs_plan* P, int32_t n_iter, nfs_iter_callback cb, v
   }
   std::vector<double> host_rho;
   if (cb) host_rho.resize((size_t)P->L * 2);
-  int done = 0;
+  int done = 0, aborted = 0;
   CGState st{};
   for (int n = 1; n <= n_iter; ++n) {
     if (gexec) NFS_CUDA(cudaGraphLaunch(gexec, P->stream));
@@ -830,7 +830,10 @@ extern "C" int nfs_cg_solve(nfs_plan* P, int32_t n_iter, nfs_iter_callback cb, v
       NFS_CUDA(cudaStreamSynchronize(P->stream));
       if (st.err || st.iter < n) break;
       NFS_CUDA(cudaMemcpy(host_rho.data(), P->d_rho, P->L * sizeof(double2), cudaMemcpyDeviceToHost));
-      cb(n, host_rho.data(), user);
+      if (cb(n, host_rho.data(), user) != 0) {
+        aborted = n;
+        break;
+      }
       if (st.stop) break;
     }
   }
@@ -843,6 +846,10 @@ extern "C" int nfs_cg_solve(nfs_plan* P, int32_t n_iter, nfs_iter_callback cb, v
     return fail(NFS_ERR_BREAKDOWN, "CG breakdown at iteration " + std::to_string(st.err_iter));
   if (st.err == NFS_ERR_NONFINITE_ITERATE)
     return fail(NFS_ERR_NONFINITE_ITERATE, "non-finite iterate at iteration " + std::to_string(st.err_iter));
+  if (aborted) {
+    if (n_done) *n_done = aborted;
+    return fail(NFS_ERR_ABORTED, "solve aborted by the iteration callback at iteration " + std::to_string(aborted));
+  }
   if (rho) NFS_CUDA(cudaMemcpy(rho, P->d_rho, P->L * sizeof(double2), cudaMemcpyDeviceToHost));
   if (done > 0) {
     if (res_norms) NFS_CUDA(cudaMemcpy(res_norms, P->d_res, done * sizeof(double), cudaMemcpyDeviceToHost));

@@ -328,6 +328,19 @@ def apply_EH(sigma: np.ndarray, sens: np.ndarray, phase) -> np.ndarray:
 # reconstruction drivers
 # ----------------------------------------------------------------------------------
 
+# Result classes: ours by default; `dispatch.install()` swaps in the reference's ReconImage /
+# CGLog so callers of the reference API get the reference's own types back.
+RESULT_TYPES = {"ReconImage": ReconImage, "CGLog": CGLog}
+
+
+def _n_samples(inputs) -> int:   # duck-typed: the reference's EncodingInputs has no properties
+    return int(inputs.sigma.shape[0])
+
+
+def _n_voxels(inputs) -> int:
+    return int(inputs.spatial.shape[1])
+
+
 def _dist_info():
     try:
         import torch.distributed as dist
@@ -347,6 +360,9 @@ def shard_rows(n_samples: int, rank: int, world: int):
 
 def _nccl_unique_id(dist, rank):
     """Rank 0 creates an NCCL unique id (via torch's bundled NCCL) and broadcasts it."""
+    import torch
+    if torch.cuda.is_available():   # torch's NCCL collectives act on its current device
+        torch.cuda.set_device(default_device())
     obj = [None]
     if rank == 0:
         import torch.cuda.nccl as tnccl
@@ -360,10 +376,10 @@ def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label:
 
     `shard=False` solves the whole problem on this rank (independent slices, recon_slices)."""
     dist, rank, world = _dist_info() if shard else (None, 0, 1)
-    lo, hi = shard_rows(inputs.n_samples, rank, world)
+    lo, hi = shard_rows(_n_samples(inputs), rank, world)
     device = default_device()
     t0 = time.perf_counter()
-    plan = _native.Plan(hi - lo, inputs.n_voxels, inputs.sens.shape[1],
+    plan = _native.Plan(hi - lo, _n_voxels(inputs), inputs.sens.shape[1],
                         inputs.spatial.shape[0], precision, device)
     try:
         if world > 1:
@@ -422,10 +438,10 @@ def _finalize(rho_r: np.ndarray, inputs: EncodingInputs, log: CGLog) -> ReconIma
     log.add_timing("apply_intensity", time.perf_counter() - t0)
     if inputs.kfilter is not None:
         t0 = time.perf_counter()
-        full = apply_filter(full, inputs.kfilter, inputs.grid)
+        full = apply_filter(full, inputs.kfilter, inputs.grid, device=default_device())
         log.add_timing("apply_kfilter", time.perf_counter() - t0)
     res = log.residual_norms[-1] if log.residual_norms else 0.0
-    return ReconImage(values=full, iterations=inputs.n_iter, final_residual=res)
+    return RESULT_TYPES["ReconImage"](values=full, iterations=inputs.n_iter, final_residual=res)
 
 
 def recon_full(inputs: EncodingInputs, memory_budget_bytes: int | None = None, callback=None,
@@ -436,7 +452,7 @@ def recon_full(inputs: EncodingInputs, memory_budget_bytes: int | None = None, c
     (K * L_R * 16 bytes > budget -> MemoryBudgetError) is kept because callers and the
     CLI exit codes depend on it.  `callback(n, rho_restricted)` runs after each iteration.
     """
-    need = inputs.n_samples * inputs.n_voxels * 16
+    need = _n_samples(inputs) * _n_voxels(inputs) * 16
     if memory_budget_bytes is not None and need > memory_budget_bytes:
         raise MemoryBudgetError(
             f"phase matrix needs {need} bytes (> budget {memory_budget_bytes}); use the split variant")
@@ -451,7 +467,7 @@ def _check_samples(inputs: EncodingInputs, shard: bool):
 
 
 def _recon_full(inputs: EncodingInputs, callback, precision, shard: bool):
-    log = CGLog()
+    log = RESULT_TYPES["CGLog"]()
     _check_samples(inputs, shard)
     plan = _make_plan(inputs, precision or default_precision(), log, timing_label=True, shard=shard)
     try:
@@ -472,20 +488,38 @@ def recon_slices(inputs_list, memory_budget_bytes: int | None = None, *, precisi
     """
     dist, rank, world = _dist_info()
     out = [None] * len(inputs_list)
+    failures = {}
     for i, inputs in enumerate(inputs_list):
         if i % world != rank:
             continue
-        need = inputs.n_samples * inputs.n_voxels * 16
-        if memory_budget_bytes is not None and need > memory_budget_bytes:
-            raise MemoryBudgetError(
-                f"phase matrix needs {need} bytes (> budget {memory_budget_bytes}); use the split variant")
-        out[i] = _recon_full(inputs, None, precision, shard=False)
-    if gather and world > 1:
+        try:
+            need = _n_samples(inputs) * _n_voxels(inputs) * 16
+            if memory_budget_bytes is not None and need > memory_budget_bytes:
+                raise MemoryBudgetError(
+                    f"phase matrix needs {need} bytes (> budget {memory_budget_bytes}); use the split variant")
+            out[i] = _recon_full(inputs, None, precision, shard=False)
+        except Exception as exc:   # no rank may skip the gather below (it would deadlock the others)
+            failures[i] = exc
+            if world == 1:
+                raise
+    if world > 1:
+        # every rank reaches this collective, failed or not; the first failure (lowest slice
+        # index) is re-raised on every rank
         parts = [None] * world
-        dist.all_gather_object(parts, {i: r for i, r in enumerate(out) if r is not None})
-        for part in parts:
+        mine = {i: r for i, r in enumerate(out) if r is not None} if gather else {}
+        dist.all_gather_object(parts, (mine, {i: (type(e), str(e)) for i, e in failures.items()}))
+        errs = {}
+        for part, fails in parts:
+            errs.update(fails)
             for i, r in part.items():
                 out[i] = r
+        if errs:
+            i = min(errs)
+            if i in failures:
+                raise failures[i]
+            cls, msg = errs[i]
+            raise (cls if isinstance(cls, type) and issubclass(cls, EngineError) else EngineError)(
+                f"slice {i} failed on another rank: {msg}")
     return out
 
 
@@ -497,7 +531,7 @@ def recon_split(inputs: EncodingInputs, callback=None, *, precision: str | None 
     """
     if inputs.block_starts is None:
         raise EngineError("split reconstruction needs block starts")
-    log = CGLog()
+    log = RESULT_TYPES["CGLog"]()
     _check_samples(inputs, True)
     plan = _make_plan(inputs, precision or default_precision(), log, timing_label=False)
     try:

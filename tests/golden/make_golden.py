@@ -212,6 +212,97 @@ def case_config_b_rows():
          EH_rows=engine.apply_EH(sig, sens, phase).astype(np.complex128))
 
 
+def config_b_problem():
+    """Config B from the reference generators: tables, S, j, phantom."""
+    grid = Grid((256, 256, 1), (0.22, 0.22, 0.002))
+    traj = simulate.make_spiral(65536, turns=32, k_max=np.pi * 256 / 0.22, readout_s=0.0715)
+    c = grid_coordinates(grid)
+    mask = np.hypot(c[:, 0], c[:, 1]) <= 0.45 * 0.22
+    harm = simulate.solid_harmonics(3, c[mask], ndim=2)
+    k_nyq = np.pi * 256 / 0.22
+    t = traj[:, 0]
+    extra = np.column_stack([0.05 * k_nyq / 0.11 ** (1 if p < 5 else 2)
+                             * np.sin(2 * np.pi * (p + 1) * t / t[-1]) for p in range(13)])
+    b0 = simulate.make_b0(grid, "linear", 200.0)
+    spatial = np.vstack([b0[mask][None], harm.T])
+    temporal = np.column_stack([traj, extra])
+    sens_full = simulate.synth_coils(grid, 32)
+    j = sensmaps.intensity_correction(sens_full, mask)[mask]
+    rho, _ = simulate.make_phantom(grid, "discs", smooth_phase=True)
+    return grid, mask, spatial, temporal, sens_full[mask], j, rho[mask]
+
+
+def blocked_forward(rho, sens, spatial, temporal, budget=2 ** 28):
+    """sigma = E rho through the reference's own phase_block / apply_E, block by block."""
+    starts = engine.choose_block_starts(temporal.shape[0], spatial.shape[1], budget)
+    out = [engine.apply_E(rho, sens, engine.phase_block(temporal[lo:hi], spatial))
+           for lo, hi in zip(starts[:-1], starts[1:])]
+    return np.concatenate(out, axis=0)
+
+
+def case_config_b_cg():
+    """Config B CG through the reference recon_split (nfs/engine.py:182-241) with the
+    pipeline's 2^28-byte blocks (nfs/pipeline.py:221), 10 iterations, noiseless phantom
+    data (sigma = E rho_true with the unnormalised coil maps).  ~40 min of CPU."""
+    grid, mask, spatial, temporal, sens, j, rho = config_b_problem()
+    sigma = blocked_forward(rho, sens, spatial, temporal)
+    starts = engine.choose_block_starts(temporal.shape[0], spatial.shape[1], 2 ** 28)
+    inputs = engine.EncodingInputs(sigma=sigma, spatial=spatial, temporal=temporal, sens=sens,
+                                   intensity=j, kfilter=None, mask_r=mask, grid=grid,
+                                   n_iter=10, block_starts=starts)
+    rho_log = {}
+    img, log = engine.recon_split(inputs, callback=lambda n, r: rho_log.__setitem__(n, r.copy()))
+    iters = np.array([1, 5, 10])
+    rows = np.arange(0, 65536, 2048) + 5
+    save("config_b_cg", mask=mask, spatial_digest=np.array(digest(spatial)),
+         temporal_digest=np.array(digest(temporal)), sens_digest=np.array(digest(sens)),
+         j_rows=j[::509], rho_true=rho, sigma_rows=sigma[rows], rows=rows, starts=starts,
+         iters=iters, rho_iters=np.stack([rho_log[i] for i in iters]), values=img.values,
+         res=np.array(log.residual_norms), sol=np.array(log.solution_norms))
+
+
+def config_d_problem(scale=4):
+    """Config D scaled down in every axis by `scale`: 3D stack of spirals,
+    order-3 solid harmonics (P+1 = 16), 32 coils, ellipsoid mask (~50 %), built from the
+    reference generators the way nfs/pipeline.py:21-117 assembles a 3D problem."""
+    nxy, nz = 128 // scale, 64 // scale
+    grid = Grid((nxy, nxy, nz), (0.22, 0.22, 0.128))
+    traj = simulate.make_spiral(4682 // scale ** 2, turns=9.14 / scale, k_max=np.pi * nxy / 0.22,
+                                readout_s=0.03, ndim=3, n_planes=nz, kz_max=np.pi * nz / 0.128)
+    c = grid_coordinates(grid)
+    mask = (c[:, 0] / 0.11) ** 2 + (c[:, 1] / 0.11) ** 2 + (c[:, 2] / 0.064) ** 2 <= 0.98
+    harm = simulate.solid_harmonics(3, c[mask], ndim=3)
+    k_nyq = np.pi * min(n / f for n, f in zip(grid.dims, grid.fov_m))
+    half = min(grid.fov_m) / 2
+    t = traj[:, 0]
+    extra = np.column_stack([0.05 * k_nyq / half ** (1 if p < 5 else 2)
+                             * np.sin(2 * np.pi * (p + 1) * t / t[-1]) for p in range(12)])
+    b0 = simulate.make_b0(grid, "linear", 200.0)
+    spatial = np.vstack([b0[mask][None], harm.T])
+    temporal = np.column_stack([traj, extra])
+    sens_full = simulate.synth_coils(grid, 32)
+    j = sensmaps.intensity_correction(sens_full, mask)[mask]
+    rho, _ = simulate.make_phantom(grid, "discs", smooth_phase=True)
+    return grid, mask, spatial, temporal, sens_full[mask], j, rho[mask]
+
+
+def case_config_d_small():
+    """Config D at 32x32x16 (scale 4): 32 coils, P+1 = 16, 50 CG iterations through the
+    reference recon_full (nfs/engine.py:125-179) -- SURVEY 8d's full-iteration 3D parity."""
+    grid, mask, spatial, temporal, sens, j, rho = config_d_problem(4)
+    sigma = blocked_forward(rho, sens, spatial, temporal)
+    inputs = engine.EncodingInputs(sigma=sigma, spatial=spatial, temporal=temporal, sens=sens,
+                                   intensity=j, kfilter=None, mask_r=mask, grid=grid, n_iter=50)
+    rho_log = {}
+    img, log = engine.recon_full(inputs, callback=lambda n, r: rho_log.__setitem__(n, r.copy()))
+    iters = np.array([1, 5, 10, 20, 30, 50])
+    save("config_d_small", mask=mask, spatial_digest=np.array(digest(spatial)),
+         temporal_digest=np.array(digest(temporal)), sens_digest=np.array(digest(sens)),
+         j=j, rho_true=rho, sigma=sigma.astype(np.complex64), sigma_digest=np.array(digest(sigma)),
+         iters=iters, rho_iters=np.stack([rho_log[i] for i in iters]), values=img.values,
+         res=np.array(log.residual_norms), sol=np.array(log.solution_norms))
+
+
 def case_metrics():
     """nfs/metrics.py ssim / rmse (tests/test_metrics.py) on the images a convergence study
     compares: a 24x20 magnitude image vs a reference, with and without a window mask."""

@@ -85,7 +85,7 @@ def _slices_worker(rank, world, port, out_dir):
     n = 7
 
     class Fake(int):   # stands in for EncodingInputs (size checks only)
-        n_samples, n_voxels = 3, 5
+        sigma, spatial = np.zeros((3, 1)), np.zeros((1, 5))
 
     out = engine.recon_slices([Fake(i) for i in range(n)])
     np.save(os.path.join(out_dir, f"slices{rank}.npy"),
@@ -105,3 +105,42 @@ def test_recon_slices_replicas_without_collective(tmp_path):
         assert np.array_equal(got[:, 0], np.arange(7)) and np.array_equal(got[:, 2], np.arange(7))
         assert np.array_equal(got[:, 1], np.arange(7) % world)      # solved by rank i mod world
         assert np.array_equal(np.load(tmp_path / f"calls{r}.npy"), np.arange(r, 7, world))
+
+
+def _slices_fail_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_09233_b200 import engine
+
+    def fake_recon(inputs, callback, precision, shard):
+        if int(inputs) == 3:   # slice 3 (rank 1) fails inside its solve, e.g. non-finite data
+            raise engine.EngineError("raw data contains non-finite values")
+        return ("image", int(inputs), rank), ("log", int(inputs))
+
+    engine._recon_full = fake_recon
+
+    class Fake(int):
+        sigma, spatial = np.zeros((3, 1)), np.zeros((1, 5))
+
+    try:
+        engine.recon_slices([Fake(i) for i in range(6)])
+        msg = "no error"
+    except engine.EngineError as exc:
+        msg = f"{type(exc).__name__}: {exc}"
+    with open(os.path.join(out_dir, f"err{rank}.txt"), "w") as f:
+        f.write(msg)
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_recon_slices_failure_reaches_every_rank(tmp_path):
+    """A slice failing on one rank must not leave the others blocked in the result gather
+    (ADVICE r1): every rank raises, the owner its own exception, the others an EngineError
+    naming the slice."""
+    world = 2
+    port = _free_port()
+    mp.spawn(_slices_fail_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    e0 = (tmp_path / "err0.txt").read_text()
+    e1 = (tmp_path / "err1.txt").read_text()
+    assert e1 == "EngineError: raw data contains non-finite values"
+    assert e0.startswith("EngineError: slice 3 failed on another rank"), e0

@@ -1,0 +1,147 @@
+"""CG-level parity at the benchmarked config B and at the north-star 3D shape.
+
+Golden iterates come from the REAL reference (tests/golden/make_golden.py):
+  config_b_cg     -- reference `recon_split` (nfs/engine.py:182-241) with the pipeline's 2^28-byte
+                     blocks (nfs/pipeline.py:221), config B (256^2 disc mask, 32 coils, P+1 = 16,
+                     K = 65,536), 10 iterations, noiseless phantom data;
+  config_d_small  -- reference `recon_full` (nfs/engine.py:125-179), config D scaled to
+                     32x32x16 (3D stack of spirals, 32 coils, P+1 = 16, ellipsoid mask), 50 it.
+The raw data of both is synthesised here by the device forward operator in FP64 (E rho_true)
+and checked against the reference's samples first (config B: 32 rows; config D: all rows),
+so the solves see the reference's inputs to ~1e-14.
+
+Stated tolerances (relative-L2 of the restricted iterate vs the reference at the same n):
+  fp64            <= 1e-8 at every stored iteration;
+  fast modes      <= 1e-5 at n <= 10, residual norms <= 1e-4 over the first 10;
+  fast modes, 3D  the 50-iteration image within the FP32 loss-of-orthogonality floor (1e-2).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+from paper_2604_09233_b200 import engine, simulate  # noqa: E402
+from paper_2604_09233_b200._native import Plan  # noqa: E402
+
+FAST = ["fp32", "f16x3", "tf32x3"]
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+def digest(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _device_sigma(prob, rho):
+    """sigma = E rho with the unnormalised coil maps, FP64 device forward."""
+    k, l = prob.temporal.shape[0], prob.spatial.shape[1]
+    plan = Plan(k, l, prob.sens.shape[1], prob.spatial.shape[0], "fp64")
+    try:
+        plan.set_tables(prob.temporal, prob.spatial)
+        plan.set_sens(prob.sens)
+        return plan.apply_E(rho)
+    finally:
+        plan.close()
+
+
+_cache = {}
+
+
+def problem_d():
+    if "D" not in _cache:
+        g = golden("config_d_small")
+        prob = simulate.make_problem("D", scale=4)
+        assert digest(prob.spatial) == str(g["spatial_digest"])
+        assert digest(prob.temporal) == str(g["temporal_digest"])
+        assert digest(prob.sens) == str(g["sens_digest"])
+        assert np.array_equal(prob.mask_r, g["mask"])
+        assert np.allclose(prob.intensity, g["j"], rtol=1e-14)
+        sigma = _device_sigma(prob, g["rho_true"])
+        assert rel(sigma, g["sigma"]) < 1e-6          # the golden keeps a complex64 copy
+        _cache["D"] = (g, prob, sigma)
+    return _cache["D"]
+
+
+def problem_b():
+    if "B" not in _cache:
+        g = golden("config_b_cg")
+        prob = simulate.make_problem("B")
+        assert digest(prob.spatial) == str(g["spatial_digest"])
+        assert digest(prob.temporal) == str(g["temporal_digest"])
+        assert digest(prob.sens) == str(g["sens_digest"])
+        assert np.array_equal(prob.mask_r, g["mask"])
+        assert np.allclose(prob.intensity[::509], g["j_rows"], rtol=1e-14)
+        sigma = _device_sigma(prob, g["rho_true"])
+        assert rel(sigma[g["rows"]], g["sigma_rows"]) < 1e-12
+        _cache["B"] = (g, prob, sigma)
+    return _cache["B"]
+
+
+def _solve(g, prob, sigma, prec, n_iter, split):
+    seen = {}
+    inputs = engine.EncodingInputs(sigma=sigma, spatial=prob.spatial, temporal=prob.temporal,
+                                   sens=prob.sens, intensity=prob.intensity, kfilter=None,
+                                   mask_r=prob.mask_r, grid=prob.grid, n_iter=n_iter,
+                                   block_starts=g["starts"] if split else None)
+    run = engine.recon_split if split else engine.recon_full
+    img, log = run(inputs, callback=lambda n, r: seen.__setitem__(n, r), precision=prec)
+    return img, log, seen
+
+
+# ------------------------------------------------------------------ 3D, 32 coils, P+1 = 16, 50 it
+def test_config_d_small_fp64_50_iterations():
+    g, prob, sigma = problem_d()
+    img, log, seen = _solve(g, prob, sigma, "fp64", 50, split=False)
+    for it, ref in zip(g["iters"], g["rho_iters"]):
+        assert rel(seen[int(it)], ref) < 1e-8, it
+    assert rel(img.values, g["values"]) < 1e-8
+    assert np.allclose(log.residual_norms, g["res"], rtol=1e-8)
+    assert np.allclose(log.solution_norms, g["sol"], rtol=1e-8)
+
+
+@pytest.mark.parametrize("prec", FAST)
+def test_config_d_small_fast_modes(prec):
+    g, prob, sigma = problem_d()
+    img, log, seen = _solve(g, prob, sigma, prec, 50, split=False)
+    its = {int(i): rel(seen[int(i)], ref) for i, ref in zip(g["iters"], g["rho_iters"])}
+    assert its[1] < 1e-5 and its[5] < 1e-5 and its[10] < 1e-5, its
+    res = np.abs(np.array(log.residual_norms[:10]) - g["res"][:10]) / g["res"][:10]
+    assert res.max() < 1e-4, res
+    assert rel(img.values, g["values"]) < 1e-2, its
+
+
+# ------------------------------------------------------------------ config B, recon_split, 10 it
+@pytest.fixture(scope="module")
+def have_b():
+    try:
+        golden("config_b_cg")
+    except FileNotFoundError:
+        pytest.fail("tests/golden/config_b_cg.npz missing (make_golden.py config_b_cg)")
+
+
+def test_config_b_fp64_recon_split(have_b):
+    g, prob, sigma = problem_b()
+    img, log, seen = _solve(g, prob, sigma, "fp64", 10, split=True)
+    for it, ref in zip(g["iters"], g["rho_iters"]):
+        assert rel(seen[int(it)], ref) < 1e-8, it
+    assert rel(img.values, g["values"]) < 1e-8
+    assert np.allclose(log.residual_norms, g["res"], rtol=1e-8)
+
+
+@pytest.mark.parametrize("prec", FAST)
+def test_config_b_fast_modes(have_b, prec):
+    """The benchmarked configuration at the production launch shape (full size: split-K and
+    multicast clusters exactly as bench.py runs them)."""
+    g, prob, sigma = problem_b()
+    img, log, seen = _solve(g, prob, sigma, prec, 10, split=True)
+    its = {int(i): rel(seen[int(i)], ref) for i, ref in zip(g["iters"], g["rho_iters"])}
+    assert max(its.values()) < 1e-5, its
+    res = np.abs(np.array(log.residual_norms) - g["res"]) / g["res"]
+    assert res.max() < 1e-4, res
+    assert rel(img.values, g["values"]) < 1e-5

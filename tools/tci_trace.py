@@ -13,6 +13,8 @@ plan.apply_EHE(prob.rho_true)
 plan.kernel_times(1)
 a = np.ctypeslib.as_array(tr, shape=(64, 12)).copy()
 a -= a[0, 0]
-print("chunk phIssued itStart emptyAok genArrA cmmaGo cmmaCommit | pfWait pfGot mathEnd phEmptyArr")
+print("chunk phIssued itStart emptyAok genArrA cmmaGo cmmaCommit | pfWait pfGot mathEnd phEmptyArr | dEmptyOk drainDone")
 for c in range(24):
-    print(c, *a[c][:6], '|', *a[c][6:10])
+    print(c, *a[c][:6], '|', *a[c][6:10], '|', *a[c][10:12])
+d = np.diff(a[4:60, 4])
+print("mean cycles per chunk (issuer start to start):", d.mean())
