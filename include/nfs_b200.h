@@ -126,6 +126,11 @@ int nfs_cg_solve(nfs_plan* plan, int32_t n_iter, nfs_iter_callback cb, void* use
  * events on the plan stream over `reps` applies: [fwd, fwd_reduce, adj, adj_reduce]. */
 int nfs_apply_EHE_resident(nfs_plan* plan, int32_t n_applies);
 int nfs_kernel_times(nfs_plan* plan, int32_t reps, float* ms_out);
+/* Timed benchmark steps (bench.py): n applies of E^H E on the device-resident p, each after a
+ * flush_bytes device write (L2 eviction, outside the timing); step_ms[n] = each apply's duration,
+ * kern_ms[2] = summed durations of the forward / adjoint main contraction kernel over the same
+ * steps (CUDA events around each launch on the plan stream). */
+int nfs_bench_applies(nfs_plan* plan, int32_t n, int64_t flush_bytes, float* step_ms, float* kern_ms);
 /* Number of kernel launches one E^H E apply issues (for the bench's launch count). */
 int nfs_launches_per_apply(nfs_plan* plan);
 /* Human-readable kernel configuration (tile sizes, splits), for logs. */

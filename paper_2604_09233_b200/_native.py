@@ -57,6 +57,8 @@ SIGNATURES = {
                                         ctypes.POINTER(ctypes.c_uint8)]),
     "nfs_ssim_log": (_c_i32, [_c_void_p, _c_dbl_p, _c_i32]),
     "nfs_kernel_times": (_c_i32, [_c_void_p, _c_i32, ctypes.POINTER(ctypes.c_float)]),
+    "nfs_bench_applies": (_c_i32, [_c_void_p, _c_i32, _c_i64, ctypes.POINTER(ctypes.c_float),
+                                   ctypes.POINTER(ctypes.c_float)]),
     "nfs_launches_per_apply": (_c_i32, [_c_void_p]),
     "nfs_plan_describe": (ctypes.c_char_p, [_c_void_p]),
     "nfs_last_error": (ctypes.c_char_p, []),
@@ -284,6 +286,13 @@ class Plan:
         out = (ctypes.c_float * 4)()
         _check(self._lib.nfs_kernel_times(self._h, int(reps), out))
         return list(out)
+
+    def bench_applies(self, n: int, flush_bytes: int = 256 << 20):
+        """(per-step ms list, summed forward / adjoint main-kernel ms) over n timed applies."""
+        steps = (ctypes.c_float * max(int(n), 1))()
+        kern = (ctypes.c_float * 2)()
+        _check(self._lib.nfs_bench_applies(self._h, int(n), int(flush_bytes), steps, kern))
+        return list(steps)[:int(n)], list(kern)
 
     def launches_per_apply(self) -> int:
         return int(self._lib.nfs_launches_per_apply(self._h))

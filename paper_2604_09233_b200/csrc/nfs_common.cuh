@@ -15,6 +15,22 @@
 
 namespace nfs {
 
+// Benchmark hook: when `on`, the main contraction kernel of each operator is bracketed by CUDA
+// events on its launch stream (ev[0]/ev[1] forward, ev[2]/ev[3] adjoint), so nfs_bench_applies
+// measures the dominant kernel inside the same timed steps as the whole apply.
+struct KernelEvents {
+  cudaEvent_t ev[4];
+  int on;
+};
+inline KernelEvents& kernel_events() {
+  static thread_local KernelEvents k{};
+  return k;
+}
+inline void kev_record(int i, cudaStream_t st) {
+  KernelEvents& k = kernel_events();
+  if (k.on) cudaEventRecord(k.ev[i], st);
+}
+
 // Device buffers come from the device's default stream-ordered memory pool with the release
 // threshold raised, so the next plan of a CG solve (or the next recon call) reuses freed
 // memory instead of paying cudaMalloc/cudaFree page-mapping costs (tens to hundreds of ms for

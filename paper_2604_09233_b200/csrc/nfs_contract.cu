@@ -409,7 +409,10 @@ cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st) {
   dim3 block(L.prec == NFS_PREC_FP64 ? kBlockD : kBlockF);
   ContractLaunch copy = L;
   void* args[] = {&copy};
-  return cudaLaunchKernel(k, grid, block, args, 0, st);
+  kev_record(L.forward ? 0 : 2, st);
+  const cudaError_t e = cudaLaunchKernel(k, grid, block, args, 0, st);
+  kev_record(L.forward ? 1 : 3, st);
+  return e;
 }
 
 void contract_kernel_shape(int prec, bool forward, int nc, int nt, int* own_per_cta,

@@ -63,6 +63,7 @@ struct NcclApi {
   pf_allreduce allreduce = nullptr;
   pf_destroy destroy = nullptr;
   pf_errstr errstr = nullptr;
+  int (*count)(void*, int*) = nullptr;
 };
 
 static NcclApi& nccl_api() {
@@ -77,6 +78,7 @@ static NcclApi& nccl_api() {
       api.allreduce = (pf_allreduce)dlsym(h, "ncclAllReduce");
       api.destroy = (pf_destroy)dlsym(h, "ncclCommDestroy");
       api.errstr = (pf_errstr)dlsym(h, "ncclGetErrorString");
+      api.count = (int (*)(void*, int*))dlsym(h, "ncclCommCount");
       api.ok = api.init_rank && api.allreduce && api.destroy;
     }
   }
@@ -325,6 +327,9 @@ extern "C" int nfs_plan_attach_comm(nfs_plan* P, const void* uid, int32_t rank, 
   if (r != 0) return fail(NFS_ERR_NCCL, std::string("ncclCommInitRank: ") + (api.errstr ? api.errstr(r) : "?"));
   P->rank = rank;
   P->world = world;
+  int n = -1;
+  if (api.count) api.count(P->comm, &n);   // the communicator's own rank count, for the logs
+  P->desc += " [nccl comm rank " + std::to_string(rank) + " of " + std::to_string(n) + "]";
   return NFS_OK;
 }
 
@@ -878,6 +883,54 @@ extern "C" int nfs_apply_EHE_resident(nfs_plan* P, int32_t n) {
   NFS_TRY(need_ready(P));
   for (int i = 0; i < n; ++i) NFS_TRY(run_ehe(P, P->d_p, P->d_q, nullptr));
   return NFS_OK;
+}
+
+// Benchmark steps: n E^H E applies on the resident p, each preceded by a device write of
+// flush_bytes (evicts L2; outside the timed events) and timed with CUDA events on the plan
+// stream: step_ms[i] = the whole apply (both operators, reductions, the NCCL all-reduce when a
+// communicator is attached); kern_ms[0] / [1] = summed durations of the forward / adjoint main
+// contraction kernel over the n steps (events around each launch, same timed steps).
+extern "C" int nfs_bench_applies(nfs_plan* P, int32_t n, int64_t flush_bytes, float* step_ms, float* kern_ms) {
+  NFS_TRY(need_ready(P));
+  if (n < 1 || !step_ms || !kern_ms || flush_bytes < 0) return fail(NFS_ERR_INVALID, "bad arguments");
+  void* flush = nullptr;
+  if (flush_bytes > 0) NFS_CUDA(nfs::dev_alloc(&flush, (size_t)flush_bytes));
+  std::vector<cudaEvent_t> ev((size_t)n * 6);
+  int status = NFS_OK;
+  for (auto& e : ev) {
+    if (cudaEventCreate(&e) != cudaSuccess) { status = fail(NFS_ERR_CUDA, "cudaEventCreate"); break; }
+  }
+  nfs::KernelEvents& kev = nfs::kernel_events();
+  for (int i = 0; i < n && status == NFS_OK; ++i) {
+    if (flush) cudaMemsetAsync(flush, i & 0xff, (size_t)flush_bytes, P->stream);
+    cudaEvent_t* e = &ev[(size_t)i * 6];
+    for (int k = 0; k < 4; ++k) kev.ev[k] = e[1 + k];
+    kev.on = 1;
+    cudaEventRecord(e[0], P->stream);
+    status = run_ehe(P, P->d_p, P->d_q, nullptr);
+    cudaEventRecord(e[5], P->stream);
+    kev.on = 0;
+  }
+  kev.on = 0;
+  if (status == NFS_OK && cudaStreamSynchronize(P->stream) != cudaSuccess) status = fail(NFS_ERR_CUDA, "bench sync");
+  kern_ms[0] = kern_ms[1] = 0.f;
+  for (int i = 0; i < n && status == NFS_OK; ++i) {
+    cudaEvent_t* e = &ev[(size_t)i * 6];
+    float a = 0.f, f = 0.f, d = 0.f;
+    cudaEventElapsedTime(&a, e[0], e[5]);
+    cudaEventElapsedTime(&f, e[1], e[2]);
+    cudaEventElapsedTime(&d, e[3], e[4]);
+    step_ms[i] = a;
+    kern_ms[0] += f;
+    kern_ms[1] += d;
+  }
+  for (auto e : ev)
+    if (e) cudaEventDestroy(e);
+  if (flush) {
+    cudaStreamSynchronize(P->stream);
+    nfs::dev_free(flush);
+  }
+  return status;
 }
 
 extern "C" int nfs_kernel_times(nfs_plan* P, int32_t reps, float* ms_out) {

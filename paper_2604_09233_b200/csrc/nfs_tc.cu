@@ -16,10 +16,11 @@
 //   KIND_F16 : kind::f16, hi/lo are FP16 (B scaled by a power of two per call so its largest
 //              entry is ~2^14); half the TMEM / SMEM bytes and twice the MMA rate of TF32.
 // The TMEM accumulator is double-buffered and drained into an FP32 shared-memory accumulator
-// every SEG chunks: the tensor core's accumulation truncates (biased error ~ steps x 2^-24 of
-// |D|), which over thousands of MMAs drifted to 1.5e-4 relative error; measured on config A
-// (E^H sigma) the error scales with SEG: 2.6e-6 at 16, 1.3e-6 at 8, 6.6e-7 at 4 (FP32 path
-// 1.5e-7).  SEG = 8 costs ~3% over 16.
+// every SEG chunks, the small split products of a chunk issued before its large one: the
+// tensor core's accumulation truncates (biased error ~ steps x 2^-24 of |D|).  Measured on the
+// masked config A (CG iterate vs the reference at iteration 10, SURVEY 8d bound 1e-5): SEG = 8
+// 3.2e-5, 4: 1.5e-5, 2: 3.2e-6, 1: 1.1e-6; per-operator time 5.2 / 5.5 / 6.2 / 7.3 ms (config
+// B).  SEG = 2 (32 items between drains) meets the bound.
 //
 // Warp roles (320 threads): warps 0-7 generate A (warp w: TMEM lane quadrant w%4, half w/4
 // of each chunk's items); warps 0-3 also drain D and run the epilogue; warp 8 = bulk-copy
@@ -47,7 +48,7 @@ namespace tc {
 constexpr int IC = 16;          // streamed items per chunk (K = 32 real per chunk)
 constexpr int KC = 2 * IC;      // real K per chunk
 #ifndef NFS_TC_SEG
-#define NFS_TC_SEG 8
+#define NFS_TC_SEG 2
 #endif
 constexpr int SEG = NFS_TC_SEG; // chunks accumulated in one TMEM D buffer before it is drained
 constexpr int GPQ = 2;          // generator warps per TMEM lane quadrant (chunk c -> warp c % GPQ)
@@ -235,7 +236,8 @@ struct Args {
   const void* b_img;      // [group][chunk][2 (hi, lo)][KC x N]
   const float2* sens;     // S' [L][ldc] (adjoint epilogue)
   const float* scale;     // [1] B scale of this call (F16), device
-  float2* out;            // fwd: partial y [split][K][ldc]; adj: partial q [group*split+split][L]
+  float2* out;            // fwd: partial y [split][K][ldc]
+  double2* out_q;         // adj: partial q [group*split+split][L] (FP64)
   const int* stop;
   int unused_debug;       // (profiling switches are compile-time: NFS_TC_DEBUG)
   long long* trace;       // profiling only: per-chunk timestamps of CTA (0,0), or null
@@ -393,17 +395,17 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
 #pragma unroll
           for (int c = 0; c < NC; ++c) out[c] = make_float2(acc_row[c * 128] * inv, acc_row[(NC + c) * 128] * inv);
         } else {
-          float qx = 0.f, qy = 0.f;
+          double qx = 0.0, qy = 0.0;   // FP64 coil combine and partial (nfs_tci.cu)
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             const float2 sv = a.sens[o * a.ldc + c0 + c];   // conj(S') * acc
-            const float ar = acc_row[c * 128] * inv, ai = acc_row[(NC + c) * 128] * inv;
-            qx = fmaf(sv.x, ar, qx);
-            qx = fmaf(sv.y, ai, qx);
-            qy = fmaf(sv.x, ai, qy);
-            qy = fmaf(-sv.y, ar, qy);
+            const double ar = acc_row[c * 128], ai = acc_row[(NC + c) * 128];
+            qx = fma((double)sv.x, ar, qx);
+            qx = fma((double)sv.y, ai, qx);
+            qy = fma((double)sv.x, ai, qy);
+            qy = fma(-(double)sv.y, ar, qy);
           }
-          a.out[(int64_t)blockIdx.y * a.n_own + o] = make_float2(qx, qy);
+          a.out_q[(int64_t)blockIdx.y * a.n_own + o] = make_double2(qx * (double)inv, qy * (double)inv);
         }
       }
     }
@@ -445,14 +447,20 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
         const uint32_t d_tmem = tbase + db * 64;
         const uint32_t bhi = smem_u32(sB + sb * B_STAGE_BYTES), blo = bhi + B_IMG_BYTES;
         const uint32_t ahi = tbase + A_COL0 + sa * (2 * ACOLS), alo = ahi + ACOLS;
+        // small split products first (while |D| is small), then the large Ah Bh: the truncating
+        // accumulation then adds the large terms KSTEPS times per chunk only (nfs_tci.cu)
 #pragma unroll
         for (int t = 0; t < KSTEPS; ++t) {
           if (TC_DEBUG & 2) break;
           const uint32_t boff = (uint32_t)(2 * t) * LBO;
           const uint32_t acc = (c % SEG != 0 || t > 0) ? 1u : 0u;
-          mma_ts<F16>(d_tmem, ahi + COLS_PER_STEP * t, smem_desc(bhi + boff, LBO, SBO), idesc, acc);
-          mma_ts<F16>(d_tmem, ahi + COLS_PER_STEP * t, smem_desc(blo + boff, LBO, SBO), idesc, 1u);
+          mma_ts<F16>(d_tmem, ahi + COLS_PER_STEP * t, smem_desc(blo + boff, LBO, SBO), idesc, acc);
           mma_ts<F16>(d_tmem, alo + COLS_PER_STEP * t, smem_desc(bhi + boff, LBO, SBO), idesc, 1u);
+        }
+#pragma unroll
+        for (int t = 0; t < KSTEPS; ++t) {
+          if (TC_DEBUG & 2) break;
+          mma_ts<F16>(d_tmem, ahi + COLS_PER_STEP * t, smem_desc(bhi + (uint32_t)(2 * t) * LBO, LBO, SBO), idesc, 1u);
         }
         mma_commit(&empty_a[sa]);   // A stage and B stage share the index (SB == SA)
         if (a.trace && lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 3] = clock64();
@@ -590,7 +598,8 @@ struct TcPlan {
   const float2* d_S = nullptr;  // [L][ldc]
   void *img_f = nullptr, *img_a = nullptr;
   float *tab_f = nullptr, *tab_a = nullptr;
-  float2 *part_y = nullptr, *part_q = nullptr;
+  float2* part_y = nullptr;
+  double2* part_q = nullptr;
   unsigned int* d_amax = nullptr;   // [2]
   float* d_scale = nullptr;         // [2]
   size_t smem = 0;
@@ -697,7 +706,7 @@ TcPlan* tc_create(int64_t K, int64_t L, int G, int nt, int sms, bool f16, std::s
             al((void**)&t->tab_f, (size_t)t->chunks_f * tc::IC * nt * 4) &&
             al((void**)&t->tab_a, (size_t)t->chunks_a * tc::IC * nt * 4) &&
             al((void**)&t->part_y, (size_t)t->split_f * std::max<int64_t>(K, 1) * t->ldc * 8) &&
-            al((void**)&t->part_q, (size_t)t->split_a * t->n_groups * L * 8) &&
+            al((void**)&t->part_q, (size_t)t->split_a * t->n_groups * L * 16) &&
             al((void**)&t->d_amax, 2 * sizeof(unsigned int)) && al((void**)&t->d_scale, 2 * sizeof(float));
   if (!ok) { *why = "device memory"; tc_destroy(t); return nullptr; }
   const float one[2] = {1.f, 1.f};
@@ -783,14 +792,18 @@ static cudaError_t launch_main(TcPlan* t, bool fwd, const int* stop, cudaStream_
   a.b_img = fwd ? t->img_f : t->img_a;
   a.sens = t->d_S;
   a.scale = t->d_scale + (fwd ? 0 : 1);
-  a.out = fwd ? t->part_y : t->part_q;
+  a.out = t->part_y;
+  a.out_q = t->part_q;
   a.stop = stop;
   a.trace = g_tc_trace;
   if (a.n_own <= 0) return cudaSuccess;
   void* k = tc_kernel(t->f16, t->nc, t->nt, fwd);
   dim3 grid((unsigned)((a.n_own + 127) / 128), (unsigned)(a.n_split * t->n_groups));
   void* args[] = {&a};
-  return cudaLaunchKernel(k, grid, dim3(tc::THREADS), args, t->smem, st);
+  kev_record(fwd ? 0 : 2, st);
+  const cudaError_t e = cudaLaunchKernel(k, grid, dim3(tc::THREADS), args, t->smem, st);
+  kev_record(fwd ? 1 : 3, st);
+  return e;
 }
 
 int tc_forward_parts(TcPlan* t, const double2* p, void* y, const int* stop, cudaStream_t st, int part) {
@@ -811,7 +824,7 @@ int tc_adjoint_parts(TcPlan* t, const void* y, double2* q, const int* stop, cuda
     e = launch_prep<false>(t, (const float2*)y, nullptr, stop, st);
     if (e == cudaSuccess) e = launch_main(t, false, stop, st);
   } else {
-    e = launch_reduce_image(0, t->part_q, q, t->L, t->split_a * t->n_groups, stop, st);
+    e = launch_reduce_image(1, t->part_q, q, t->L, t->split_a * t->n_groups, stop, st);
   }
   if (e != cudaSuccess) return tc_fail(std::string("tc adjoint: ") + cudaGetErrorString(e));
   return 0;

@@ -131,10 +131,14 @@ class Problem:
     n_iter: int
 
 
-def _bases(grid, b0, mask, traj, order):
-    """Spatial/temporal tables; order > 1 appends synthetic higher-order terms."""
+def _bases(grid, b0, mask, traj, order, z_offset=0.0):
+    """Spatial/temporal tables; order > 1 appends synthetic higher-order terms.  `z_offset`
+    moves a 2D slice off the isocentre (config C): the harmonics are evaluated at z = z_offset."""
     nd = grid.ndim
     coords = grid_coordinates(grid)[mask]
+    if z_offset:
+        coords = coords.copy()
+        coords[:, 2] += z_offset
     harm = solid_harmonics(order, coords, ndim=nd)
     terms = traj[:, 1:]
     if harm.shape[1] > terms.shape[1]:
@@ -194,3 +198,29 @@ def make_problem(name: str, scale: int = 1) -> Problem:
         intensity = 1.0 / np.sqrt(ssq[mask])
     return Problem(name, grid, spatial, temporal, sens_full[mask], intensity, mask,
                    rho[mask], n_iter)
+
+
+def slice_offsets(n_slices: int = 40, spacing_m: float = 0.002) -> np.ndarray:
+    """Slice centres of a multi-slice stack, symmetric about the isocentre (config C)."""
+    return spacing_m * (np.arange(n_slices) - (n_slices - 1) / 2.0)
+
+
+def make_slices(n_slices: int = 40, spacing_m: float = 0.002, scale: int = 1, which=None):
+    """Config C: a stack of `n_slices` config-B slices at z offsets +-, 2 mm apart,
+    sharing the trajectory and its field-term time courses; each slice's spatial basis holds
+    the third-order solid harmonics at ITS z (z != 0 switches on the z-dependent terms).
+    Every slice is an independent reconstruction problem (replicas across GPUs, no
+    collective).  `which` selects slice indices (default all)."""
+    base = make_problem("B", scale=scale)
+    n = 256 // scale
+    grid = base.grid
+    traj = make_spiral(65536 // scale**2, turns=32 / scale, k_max=np.pi * n / 0.22, readout_s=0.0715)
+    b0 = make_b0(grid, "linear", 200.0)
+    out = []
+    zs = slice_offsets(n_slices, spacing_m)
+    for i in (range(n_slices) if which is None else which):
+        spatial, temporal = _bases(grid, b0, base.mask_r, traj, 3, z_offset=float(zs[i]))
+        rho = base.rho_true * (0.75 + 0.5 * i / max(n_slices - 1, 1))   # slice-dependent contrast
+        out.append(Problem(f"C[{i}] z={zs[i] * 1e3:+.1f} mm", grid, spatial, temporal, base.sens,
+                           base.intensity, base.mask_r, rho, base.n_iter))
+    return out

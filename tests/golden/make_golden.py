@@ -303,6 +303,62 @@ def case_config_d_small():
          res=np.array(log.residual_norms), sol=np.array(log.solution_norms))
 
 
+def case_config_c_slice():
+    """Config C: one off-centre slice (z = +39 mm, slice 39 of a 40-slice stack at
+    2 mm spacing) of config B scaled to 64x64 (scale 4): the third-order harmonics at z != 0,
+    shared trajectory, 32 coils, slice contrast 1.25; reference recon_full, 10 iterations."""
+    scale, z = 4, 0.002 * (39 - 19.5)
+    n = 256 // scale
+    grid = Grid((n, n, 1), (0.22, 0.22, 0.002))
+    traj = simulate.make_spiral(65536 // scale ** 2, turns=32 / scale, k_max=np.pi * n / 0.22,
+                                readout_s=0.0715)
+    c = grid_coordinates(grid)
+    mask = np.hypot(c[:, 0], c[:, 1]) <= 0.45 * 0.22
+    cz = c[mask].copy()
+    cz[:, 2] += z
+    harm = simulate.solid_harmonics(3, cz, ndim=2)
+    k_nyq = np.pi * n / 0.22
+    t = traj[:, 0]
+    extra = np.column_stack([0.05 * k_nyq / 0.11 ** (1 if p < 5 else 2)
+                             * np.sin(2 * np.pi * (p + 1) * t / t[-1]) for p in range(13)])
+    b0 = simulate.make_b0(grid, "linear", 200.0)
+    spatial = np.vstack([b0[mask][None], harm.T])
+    temporal = np.column_stack([traj, extra])
+    sens_full = simulate.synth_coils(grid, 32)
+    j = sensmaps.intensity_correction(sens_full, mask)[mask]
+    rho, _ = simulate.make_phantom(grid, "discs", smooth_phase=True)
+    rho = rho[mask] * 1.25
+    sens = sens_full[mask]
+    sigma = blocked_forward(rho, sens, spatial, temporal)
+    inputs = engine.EncodingInputs(sigma=sigma, spatial=spatial, temporal=temporal, sens=sens,
+                                   intensity=j, kfilter=None, mask_r=mask, grid=grid, n_iter=10)
+    rho_log = {}
+    img, log = engine.recon_full(inputs, callback=lambda n, r: rho_log.__setitem__(n, r.copy()))
+    iters = np.array([1, 5, 10])
+    save("config_c_slice", mask=mask, spatial_digest=np.array(digest(spatial)),
+         temporal_digest=np.array(digest(temporal)), sens_digest=np.array(digest(sens)), z=np.array(z),
+         rho_true=rho, sigma=sigma.astype(np.complex64), iters=iters,
+         rho_iters=np.stack([rho_log[i] for i in iters]), values=img.values,
+         res=np.array(log.residual_norms), sol=np.array(log.solution_norms))
+
+
+def case_config_d_small_split():
+    """The reference's OWN sensitivity on the config-D-small CG: recon_split (4 row blocks) vs
+    recon_full differ only by summation order, so their iterate drift over 50 iterations is the
+    floor any other FP64 implementation can be held to."""
+    grid, mask, spatial, temporal, sens, j, rho = config_d_problem(4)
+    sigma = blocked_forward(rho, sens, spatial, temporal)
+    starts = np.linspace(0, temporal.shape[0], 5, dtype=int)
+    inputs = engine.EncodingInputs(sigma=sigma, spatial=spatial, temporal=temporal, sens=sens,
+                                   intensity=j, kfilter=None, mask_r=mask, grid=grid, n_iter=50,
+                                   block_starts=starts)
+    rho_log = {}
+    img, log = engine.recon_split(inputs, callback=lambda n, r: rho_log.__setitem__(n, r.copy()))
+    iters = np.array([1, 5, 10, 20, 30, 50])
+    save("config_d_small_split", starts=starts, iters=iters,
+         rho_iters=np.stack([rho_log[i] for i in iters]), res=np.array(log.residual_norms))
+
+
 def case_metrics():
     """nfs/metrics.py ssim / rmse (tests/test_metrics.py) on the images a convergence study
     compares: a 24x20 magnitude image vs a reference, with and without a window mask."""

@@ -4,7 +4,7 @@ Tolerances (stated per mode):
   fp64 parity mode : the reference's own tolerances (1e-14 phase, 1e-10 / 1e-12 operators,
                      1e-10 split/full, 1e-12 exact recovery) and <= 1e-8 relative-L2 on
                      the CG iterate at 20 iterations of config A.
-  fp32 fast mode   : operators <= 2e-5 relative-L2; CG iterate <= 1e-5 at 10 iterations
+  fast modes       : (fp32, f16x3, tf32x3) operators <= 2e-5 relative-L2; CG iterate <= 1e-5 at 10 iterations
                      and <= 1e-2 at 20 iterations of config A (FP32 loss-of-orthogonality
                      floor).
 """
@@ -167,18 +167,18 @@ def test_config_a_fast_mode_tolerance(prec):
                                              prob.sens, 20),
                                  callback=lambda n, r: seen.__setitem__(n, r), precision=prec)
     assert rel(seen[5], g["rho_iters"][0]) < 1e-5
-    assert rel(seen[10], g["rho_iters"][1]) < (1e-5 if prec == "fp32" else 3e-5)
-    assert rel(img.values, g["values"]) < 1e-2
-    assert np.allclose(log.residual_norms[:10], g["res"][:10], rtol=1e-3)
+    assert rel(seen[10], g["rho_iters"][1]) < 1e-5          # <= 1e-5 at <= 10 it
+    assert rel(img.values, g["values"]) < 1e-2                # <= 1e-2 at 20 it (FP32 floor)
+    assert np.allclose(log.residual_norms[:10], g["res"][:10], rtol=1e-4)
 
 
 @pytest.mark.parametrize("prec", ["fp32", "tf32x3", "f16x3"])
 def test_config_a_masked_fast_mode_tolerance(prec):
-    """Masked config A (phantom support, intensity correction, k-filter) in the fast modes: the
-    FP32-class operators track the reference to ~2e-6 at iteration 5; the CG amplifies
-    per-apply rounding from iteration ~6 on (the masked system is CG-chaotic even in FP64), so
-    iteration 10 is pinned at 1e-4 (measured: fp32 4e-6, tf32x3 3e-5, f16x3 3.6e-5 -- the
-    tensor-core accumulation truncates between drains, nfs_tci.cu) and the image at 1e-2."""
+    """Masked config A (phantom support, intensity correction, k-filter) in the fast modes, at
+    the SURVEY 8d fast-mode bound: <= 1e-5 at iteration 10 (measured: fp32 4.1e-6, f16x3 5.1e-6,
+    tf32x3 3.2e-6 -- the tensor-core modes drain their truncating TMEM accumulator every 32
+    items, nfs_tci.cu / nfs_tc.cu), residual norms within 1e-4 over the first 10 iterations,
+    and the image within the FP32 loss-of-orthogonality floor at 20 (1e-2)."""
     g = golden("config_a")
     pm = simulate.make_problem("A_mask")
     seen = {}
@@ -187,9 +187,9 @@ def test_config_a_masked_fast_mode_tolerance(prec):
                                              kfilter=g["kfilter"]),
                                  callback=lambda n, r: seen.__setitem__(n, r), precision=prec)
     assert rel(seen[5], g["rho_iters_mask"][0]) < 5e-6
-    assert rel(seen[10], g["rho_iters_mask"][1]) < 1e-4
+    assert rel(seen[10], g["rho_iters_mask"][1]) < 1e-5
     assert rel(img.values, g["values_mask"]) < 1e-2
-    assert np.allclose(log.residual_norms[:5], g["res_mask"][:5], rtol=1e-4)
+    assert np.allclose(log.residual_norms[:10], g["res_mask"][:10], rtol=1e-4)
 
 
 def test_config_a_masked_with_filter_fp64():
