@@ -83,6 +83,15 @@ int nfs_set_tables_grid(nfs_plan* plan, const double* temporal, const int64_t* v
 /* Sensitivities (L_R x G complex) and optional intensity correction j (L_R) -> S' = S o j
  * (nfs/engine.py:143).  intensity == NULL means j = 1 (apply_E / apply_EH semantics). */
 int nfs_set_sens(nfs_plan* plan, const double* sens, const double* intensity);
+/* Same from the FULL-grid maps sens_full [n_full][n_coils] (complex): the mask restriction
+ * (vox_index[L_R] = grid index of each reconstructed voxel, nfs/pipeline.py:202) and, when
+ * intensity is NULL, the intensity correction j = 1/sqrt(sum_c |S|^2) (nfs/sensmaps.py:145-152)
+ * run on the device; j_out (L_R, optional) receives the j used. */
+int nfs_set_sens_grid(nfs_plan* plan, const double* sens_full, int64_t n_full, const int64_t* vox_index,
+                      const double* intensity, double* j_out);
+/* Stateless device intensity correction of the n_r voxels vox_index of the full-grid maps. */
+int nfs_intensity_correction(int32_t device, const double* sens_full, int64_t n_full, int32_t n_coils,
+                             const int64_t* vox_index, int64_t n_r, double* j_out);
 /* Raw samples of this rank (K x G complex); non-finite -> NFS_ERR_NONFINITE. */
 int nfs_set_samples(nfs_plan* plan, const double* sigma);
 

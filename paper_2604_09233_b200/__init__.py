@@ -9,6 +9,7 @@ from .core import Grid, ReconImage, grid_coordinates
 from .engine import (
     CGLog,
     DeviceRMSE,
+    DeviceSens,
     DeviceSSIM,
     DeviceSpatial,
     EncodingInputs,
@@ -18,6 +19,7 @@ from .engine import (
     apply_EH,
     build_bases,
     choose_block_starts,
+    intensity_correction,
     phase_block,
     recon_full,
     recon_slices,
@@ -25,8 +27,8 @@ from .engine import (
 )
 
 __all__ = [
-    "CGLog", "DeviceRMSE", "DeviceSSIM", "DeviceSpatial", "EncodingInputs", "EngineError", "Grid", "MemoryBudgetError", "ReconImage",
-    "apply_E", "apply_EH", "build_bases", "choose_block_starts", "grid_coordinates",
+    "CGLog", "DeviceRMSE", "DeviceSens", "DeviceSSIM", "DeviceSpatial", "EncodingInputs", "EngineError", "Grid", "MemoryBudgetError", "ReconImage",
+    "apply_E", "apply_EH", "build_bases", "choose_block_starts", "grid_coordinates", "intensity_correction",
     "phase_block", "recon_full", "recon_slices", "recon_split",
 ]
 

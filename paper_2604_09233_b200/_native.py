@@ -42,6 +42,9 @@ SIGNATURES = {
     "nfs_set_tables_grid": (_c_i32, [_c_void_p, _c_dbl_p, ctypes.POINTER(_c_i64), _c_dbl_p,
                                      ctypes.POINTER(_c_i32), _c_dbl_p, _c_i32]),
     "nfs_set_sens": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
+    "nfs_set_sens_grid": (_c_i32, [_c_void_p, _c_dbl_p, _c_i64, ctypes.POINTER(_c_i64), _c_dbl_p, _c_dbl_p]),
+    "nfs_intensity_correction": (_c_i32, [_c_i32, _c_dbl_p, _c_i64, _c_i32, ctypes.POINTER(_c_i64), _c_i64,
+                                          _c_dbl_p]),
     "nfs_set_samples": (_c_i32, [_c_void_p, _c_dbl_p]),
     "nfs_apply_E": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
     "nfs_apply_EH": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
@@ -178,6 +181,21 @@ class Plan:
         _check(self._lib.nfs_set_sens(self._h, _dp(s.view(np.float64)),
                                       None if j is None else _dp(j)))
 
+    def set_sens_grid(self, sens_full, vox_index, intensity=None):
+        """S' from the full-grid maps: restriction (and j when intensity is None) on the device.
+        Returns the j the device used (L_R,)."""
+        _, l, g, _ = self.shape
+        full = _c128(sens_full)
+        idx = np.ascontiguousarray(vox_index, dtype=np.int64)
+        if full.ndim != 2 or full.shape[1] != g or idx.shape != (l,):
+            raise EngineError("full-grid sensitivity / voxel index shapes do not match the plan")
+        j_out = np.empty(l)
+        jin = None if intensity is None else np.ascontiguousarray(intensity, dtype=np.float64)
+        _check(self._lib.nfs_set_sens_grid(self._h, _dp(full.view(np.float64)), int(full.shape[0]),
+                                           idx.ctypes.data_as(ctypes.POINTER(_c_i64)),
+                                           None if jin is None else _dp(jin), _dp(j_out)))
+        return j_out
+
     def set_samples(self, sigma):
         k, _, g, _ = self.shape
         s = _c128(sigma, (k, g))
@@ -296,3 +314,17 @@ class Plan:
 
     def launches_per_apply(self) -> int:
         return int(self._lib.nfs_launches_per_apply(self._h))
+
+
+def intensity_correction(sens_full, vox_index, device: int = 0) -> np.ndarray:
+    """Device j = 1/sqrt(sum_c |S|^2) of the voxels `vox_index` (nfs/sensmaps.py:145-152)."""
+    lib = load_library()
+    full = _c128(sens_full)
+    idx = np.ascontiguousarray(vox_index, dtype=np.int64)
+    if full.ndim != 2:
+        raise EngineError("sensitivity maps must be (L, coils)")
+    out = np.empty(idx.size)
+    _check(lib.nfs_intensity_correction(int(device), _dp(full.view(np.float64)), int(full.shape[0]),
+                                        int(full.shape[1]), idx.ctypes.data_as(ctypes.POINTER(_c_i64)),
+                                        int(idx.size), _dp(out)))
+    return out

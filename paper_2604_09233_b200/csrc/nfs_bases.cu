@@ -110,6 +110,59 @@ __global__ void prep_sens_kernel(const double2* __restrict__ sens, const double*
   }
 }
 
+// Intensity correction on the device (nfs/sensmaps.py:145-152): for every reconstructed voxel
+// (grid index idx[l]) j = 1/sqrt(sum_c |S_c|^2) if that sum is > 0, else 0.  |S|^2 is formed as
+// abs(S)^2 with abs = hypot, like numpy's np.abs(maps) ** 2; the coil sum runs in numpy's
+// pairwise order for rows of <= 128 coils (8 interleaved partial sums, combined as
+// ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)), then the remainder sequentially), so j matches the
+// reference to the last bit up to the hypot rounding (CUDA hypot: <= 1 ulp).
+__global__ void intensity_kernel(const double2* __restrict__ full, const int64_t* __restrict__ idx, int64_t n_r,
+                                 int g, double* __restrict__ j) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n_r; l += (int64_t)gridDim.x * blockDim.x) {
+    const double2* row = full + idx[l] * g;
+    auto sq = [&](int c) {
+      const double a = hypot(row[c].x, row[c].y);
+      return a * a;
+    };
+    double ssq;
+    if (g < 8) {
+      ssq = 0.0;
+      for (int c = 0; c < g; ++c) ssq += sq(c);
+    } else {
+      double r[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = sq(k);
+      int c = 8;
+      for (; c + 8 <= g; c += 8)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] += sq(c + k);
+      ssq = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+      for (; c < g; ++c) ssq += sq(c);
+    }
+    j[l] = ssq > 0.0 ? 1.0 / sqrt(ssq) : 0.0;
+  }
+}
+
+// S' = S[idx] o j: the mask restriction as a gather of the full-grid maps (coils padded to ldc)
+template <typename T2>
+__global__ void prep_sens_gather_kernel(const double2* __restrict__ full, const int64_t* __restrict__ idx,
+                                        const double* __restrict__ j, int64_t n_r, int g, int ldc, T2* __restrict__ out) {
+  const int64_t n = n_r * ldc;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = i / ldc;
+    const int c = (int)(i - l * ldc);
+    T2 v;
+    v.x = 0; v.y = 0;
+    if (c < g) {
+      const double w = j[l];
+      const double2 s = full[idx[l] * g + c];
+      v.x = s.x * w;
+      v.y = s.y * w;
+    }
+    out[i] = v;
+  }
+}
+
 // count of non-finite doubles (raw data check of nfs_set_samples)
 __global__ void count_nonfinite_kernel(const double* __restrict__ x, int64_t n, unsigned int* out) {
   unsigned int bad = 0;
@@ -159,6 +212,20 @@ cudaError_t launch_prep_sens(const double2* d_sens, const double* d_j, int64_t L
                              void* d_out, cudaStream_t st) {
   if (fp64) prep_sens_kernel<double2><<<grid_for(L * ldc), 256, 0, st>>>(d_sens, d_j, L, g, ldc, (double2*)d_out);
   else prep_sens_kernel<float2><<<grid_for(L * ldc), 256, 0, st>>>(d_sens, d_j, L, g, ldc, (float2*)d_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_intensity(const double2* d_full, const int64_t* d_idx, int64_t n_r, int g, double* d_j,
+                             cudaStream_t st) {
+  if (n_r > 0) intensity_kernel<<<grid_for(n_r), 256, 0, st>>>(d_full, d_idx, n_r, g, d_j);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep_sens_gather(const double2* d_full, const int64_t* d_idx, const double* d_j, int64_t n_r, int g,
+                                    int ldc, bool fp64, void* d_out, cudaStream_t st) {
+  if (n_r <= 0) return cudaSuccess;
+  if (fp64) prep_sens_gather_kernel<double2><<<grid_for(n_r * ldc), 256, 0, st>>>(d_full, d_idx, d_j, n_r, g, ldc, (double2*)d_out);
+  else prep_sens_gather_kernel<float2><<<grid_for(n_r * ldc), 256, 0, st>>>(d_full, d_idx, d_j, n_r, g, ldc, (float2*)d_out);
   return cudaGetLastError();
 }
 

@@ -14,5 +14,9 @@ cudaError_t launch_prep_tables(const double* d_temporal, const double* d_spatial
                                bool spatial_lp = false);
 cudaError_t launch_prep_sens(const double2* d_sens, const double* d_j, int64_t L, int g, int ldc, bool fp64,
                              void* d_out, cudaStream_t st);
+cudaError_t launch_intensity(const double2* d_full, const int64_t* d_idx, int64_t n_r, int g, double* d_j,
+                             cudaStream_t st);
+cudaError_t launch_prep_sens_gather(const double2* d_full, const int64_t* d_idx, const double* d_j, int64_t n_r, int g,
+                                    int ldc, bool fp64, void* d_out, cudaStream_t st);
 cudaError_t launch_count_nonfinite(const double* d_x, int64_t n, unsigned int* d_out, cudaStream_t st);
 }  // namespace nfs

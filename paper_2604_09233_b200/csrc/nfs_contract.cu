@@ -211,18 +211,20 @@ __global__ void __launch_bounds__(kBlockF) contract_f32_kernel(ContractLaunch a)
         for (int c = 0; c < NC; ++c)
           out[c] = lane ? make_float2(are[pr][c].y, aim[pr][c].y) : make_float2(are[pr][c].x, aim[pr][c].x);
       } else {
-        float qx = 0.f, qy = 0.f;
+        // FP64 coil combine and partial image: rounding q to FP32 per apply is an inconsistent
+        // per-apply error the CG amplifies
+        double qx = 0.0, qy = 0.0;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           const float2 sv = sens[o * a.ldc + c0 + c];   // conj(S') * acc
-          const float ax = lane ? are[pr][c].y : are[pr][c].x;
-          const float ay = lane ? aim[pr][c].y : aim[pr][c].x;
-          qx = fmaf(sv.x, ax, qx);
-          qx = fmaf(sv.y, ay, qx);
-          qy = fmaf(sv.x, ay, qy);
-          qy = fmaf(-sv.y, ax, qy);
+          const double ax = lane ? are[pr][c].y : are[pr][c].x;
+          const double ay = lane ? aim[pr][c].y : aim[pr][c].x;
+          qx = fma((double)sv.x, ax, qx);
+          qx = fma((double)sv.y, ay, qx);
+          qy = fma((double)sv.x, ay, qy);
+          qy = fma(-(double)sv.y, ax, qy);
         }
-        static_cast<float2*>(a.out)[(int64_t)blockIdx.y * a.n_own + o] = make_float2(qx, qy);
+        static_cast<double2*>(a.out)[(int64_t)blockIdx.y * a.n_own + o] = make_double2(qx, qy);
       }
     }
   }

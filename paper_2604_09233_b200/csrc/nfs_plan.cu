@@ -242,7 +242,7 @@ extern "C" int nfs_plan_create(nfs_plan** out, int64_t n_samples, int64_t n_voxe
       (s = alloc(&P->d_sig, (size_t)K * P->ldc * t2)) ||
       (s = alloc(&P->d_y, (size_t)K * P->ldc * t2)) ||
       (s = alloc(&P->d_w, (size_t)L * P->ldc * t2)) ||
-      (s = alloc(&P->d_partq, (size_t)P->split_a * P->NG * L * t2)) ||
+      (s = alloc(&P->d_partq, (size_t)P->split_a * P->NG * L * sizeof(double2))) ||   // FP64 partial images
       (s = alloc((void**)&P->d_p, L * sizeof(double2))) ||
       (s = alloc((void**)&P->d_q, L * sizeof(double2))) ||
       (s = alloc((void**)&P->d_r, L * sizeof(double2))) ||
@@ -504,6 +504,65 @@ extern "C" int nfs_set_sens(nfs_plan* P, const double* sens, const double* inten
   return NFS_OK;
 }
 
+// S' from the FULL-grid maps (f3: the mask restriction and, with intensity == NULL, the intensity
+// correction run on the device): S'[l] = S_full[vox_index[l]] o j[l].
+extern "C" int nfs_set_sens_grid(nfs_plan* P, const double* sens_full, int64_t n_full, const int64_t* vox_index,
+                                 const double* intensity, double* j_out) {
+  if (!P || !sens_full || !vox_index || n_full < P->L) return fail(NFS_ERR_INVALID, "bad full-grid sensitivities");
+  NFS_CUDA(cudaSetDevice(P->device));
+  const int64_t L = P->L;
+  for (int64_t l = 0; l < L; ++l)
+    if (vox_index[l] < 0 || vox_index[l] >= n_full) return fail(NFS_ERR_INVALID, "voxel index outside the grid");
+  DevScratch sc{P->stream, {}};
+  double2* d_full = nullptr;
+  int64_t* d_idx = nullptr;
+  double* d_j = nullptr;
+  NFS_CUDA(sc.get(&d_full, (size_t)n_full * P->G * sizeof(double2)));
+  NFS_CUDA(sc.get(&d_idx, (size_t)L * sizeof(int64_t)));
+  NFS_CUDA(sc.get(&d_j, (size_t)L * 8));
+  NFS_CUDA(nfs::h2d(d_full, sens_full, (size_t)n_full * P->G * sizeof(double2), P->stream));
+  NFS_CUDA(cudaMemcpyAsync(d_idx, vox_index, (size_t)L * sizeof(int64_t), cudaMemcpyHostToDevice, P->stream));
+  if (intensity) NFS_CUDA(cudaMemcpyAsync(d_j, intensity, (size_t)L * 8, cudaMemcpyHostToDevice, P->stream));
+  else NFS_CUDA(nfs::launch_intensity(d_full, d_idx, L, P->G, d_j, P->stream));
+  NFS_CUDA(nfs::launch_prep_sens_gather(d_full, d_idx, d_j, L, P->G, P->ldc, P->esz == 8, P->d_S, P->stream));
+  if (j_out) NFS_CUDA(cudaMemcpyAsync(j_out, d_j, (size_t)L * 8, cudaMemcpyDeviceToHost, P->stream));
+  NFS_CUDA(cudaStreamSynchronize(P->stream));
+  P->have_sens = true;
+  if (P->tc) {
+    int s = nfs::tc_set_sens(P->tc, P->d_S, P->ldc, P->stream);
+    if (s) return fail(NFS_ERR_CUDA, "tc sens: " + std::string(nfs::tc_last_error()));
+  }
+  if (P->tci) {
+    int s = nfs::tci_set_sens(P->tci, P->d_S, P->ldc, P->stream);
+    if (s) return fail(NFS_ERR_CUDA, "tci sens: " + std::string(nfs::tci_last_error()));
+  }
+  return NFS_OK;
+}
+
+// Stateless device intensity correction (nfs/sensmaps.py:145-152) of the reconstructed voxels.
+extern "C" int nfs_intensity_correction(int32_t device, const double* sens_full, int64_t n_full, int32_t n_coils,
+                                        const int64_t* vox_index, int64_t n_r, double* j_out) {
+  if (!sens_full || !vox_index || !j_out || n_full < 0 || n_r < 0 || n_coils < 1)
+    return fail(NFS_ERR_INVALID, "bad arguments");
+  for (int64_t l = 0; l < n_r; ++l)
+    if (vox_index[l] < 0 || vox_index[l] >= n_full) return fail(NFS_ERR_INVALID, "voxel index outside the grid");
+  NFS_CUDA(cudaSetDevice(device));
+  cudaStream_t st = nfs::alloc_stream();
+  DevScratch sc{st, {}};
+  double2* d_full = nullptr;
+  int64_t* d_idx = nullptr;
+  double* d_j = nullptr;
+  NFS_CUDA(sc.get(&d_full, (size_t)n_full * n_coils * sizeof(double2)));
+  NFS_CUDA(sc.get(&d_idx, (size_t)n_r * sizeof(int64_t)));
+  NFS_CUDA(sc.get(&d_j, (size_t)n_r * 8));
+  NFS_CUDA(nfs::h2d(d_full, sens_full, (size_t)n_full * n_coils * sizeof(double2), st));
+  NFS_CUDA(cudaMemcpyAsync(d_idx, vox_index, (size_t)n_r * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  NFS_CUDA(nfs::launch_intensity(d_full, d_idx, n_r, n_coils, d_j, st));
+  NFS_CUDA(cudaMemcpyAsync(j_out, d_j, (size_t)n_r * 8, cudaMemcpyDeviceToHost, st));
+  NFS_CUDA(cudaStreamSynchronize(st));
+  return NFS_OK;
+}
+
 static int upload_samples(nfs_plan* P, const double* sigma, void* dst) {
   const size_t n = (size_t)P->K * P->G;
   NFS_TRY(ensure_io(P, std::max<size_t>(n, (size_t)P->L)));
@@ -591,7 +650,7 @@ static int run_adjoint(nfs_plan* P, const void* y, double2* q, const int* stop) 
     L.stop = stop;
     L.out = P->d_partq;
     NFS_CUDA(nfs::launch_contract(L, P->stream));
-    NFS_CUDA(nfs::launch_reduce_image(L.prec == NFS_PREC_FP64 ? 1 : 0, P->d_partq, q, P->L,
+    NFS_CUDA(nfs::launch_reduce_image(1, P->d_partq, q, P->L,
                                       P->split_a * P->NG, stop, P->stream));
   }
   if (P->comm) {   // sample-sharded: sum the adjoint images of all ranks (in place)
@@ -981,7 +1040,7 @@ extern "C" int nfs_kernel_times(nfs_plan* P, int32_t reps, float* ms_out) {
       NFS_CUDA(cudaEventRecord(e[2], P->stream));
       NFS_CUDA(nfs::launch_contract(A, P->stream));
       NFS_CUDA(cudaEventRecord(e[3], P->stream));
-      NFS_CUDA(nfs::launch_reduce_image(cp, P->d_partq, P->d_q, P->L, P->split_a * P->NG, nullptr, P->stream));
+      NFS_CUDA(nfs::launch_reduce_image(1, P->d_partq, P->d_q, P->L, P->split_a * P->NG, nullptr, P->stream));
       NFS_CUDA(cudaEventRecord(e[4], P->stream));
     }
     NFS_CUDA(cudaEventSynchronize(e[4]));

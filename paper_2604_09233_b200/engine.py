@@ -30,7 +30,7 @@ from .simulate import solid_harmonics
 __all__ = [
     "EngineError", "MemoryBudgetError", "EncodingInputs", "CGLog", "phase_block", "apply_E",
     "apply_EH", "recon_full", "recon_split", "choose_block_starts", "build_bases",
-    "default_precision", "PhaseBlock",
+    "default_precision", "PhaseBlock", "DeviceSens", "intensity_correction",
 ]
 
 
@@ -294,6 +294,57 @@ class PhaseBlock:
         return np.abs(self.materialize())
 
 
+class DeviceSens:
+    """Full-grid coil maps plus the reconstruction mask, standing in for the restricted maps
+    `sens_full[mask_r]` of EncodingInputs.sens: the mask restriction and S' = S o j
+    run on the GPU at upload (`nfs_set_sens_grid`), and `.intensity` is the intensity correction
+    j = 1/sqrt(sum_c |S|^2) of the reconstructed voxels computed on the GPU
+    (nfs/sensmaps.py:145-152, restricted as nfs/pipeline.py:203).  `np.asarray(handle)` gives the
+    host restriction, so the handle can stand in for the array anywhere."""
+
+    __array_priority__ = 10
+
+    def __init__(self, sens_full, mask_r, device: int | None = None):
+        self.sens_full = np.ascontiguousarray(sens_full, dtype=np.complex128)
+        self.mask_r = np.asarray(mask_r, dtype=bool).reshape(-1)
+        if self.sens_full.ndim != 2 or self.sens_full.shape[0] != self.mask_r.size:
+            raise EngineError("full-grid sensitivities and mask do not match")
+        self.vox_index = np.flatnonzero(self.mask_r).astype(np.int64)
+        self.device = default_device() if device is None else device
+        self._j = None
+
+    @property
+    def shape(self):
+        return (int(self.vox_index.size), int(self.sens_full.shape[1]))
+
+    @property
+    def ndim(self):
+        return 2
+
+    @property
+    def dtype(self):
+        return np.dtype(np.complex128)
+
+    def __array__(self, dtype=None, copy=None):
+        out = self.sens_full[self.mask_r]
+        return out if dtype is None else out.astype(dtype)
+
+    @property
+    def intensity(self) -> np.ndarray:
+        """j on the reconstructed voxels, evaluated on the GPU (cached)."""
+        if self._j is None:
+            self._j = _native.intensity_correction(self.sens_full, self.vox_index, self.device)
+        return self._j
+
+
+def intensity_correction(maps: np.ndarray, mask_r) -> np.ndarray:
+    """nfs/sensmaps.py:145-152 on the GPU: j = 1/sqrt(sum_coils |S|^2) on the mask, else 0."""
+    mask_r = np.asarray(mask_r, dtype=bool).reshape(-1)
+    j = np.zeros(np.asarray(maps).shape[0])
+    j[mask_r] = _native.intensity_correction(maps, np.flatnonzero(mask_r), default_device())
+    return j
+
+
 def phase_block(temporal_rows: np.ndarray, spatial: np.ndarray) -> PhaseBlock:
     """Lazy device phase block for a row range (nfs/engine.py:93-95)."""
     return PhaseBlock(temporal_rows, spatial)
@@ -386,7 +437,10 @@ def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label:
             plan.attach_comm(_nccl_unique_id(dist, rank), rank, world)
         t_plan = time.perf_counter() - t0
         t0 = time.perf_counter()
-        plan.set_sens(inputs.sens, inputs.intensity)          # S' = S o j on upload
+        if isinstance(inputs.sens, DeviceSens):              # restriction + S' = S o j on the GPU
+            plan.set_sens_grid(inputs.sens.sens_full, inputs.sens.vox_index, inputs.intensity)
+        else:
+            plan.set_sens(inputs.sens, inputs.intensity)      # S' = S o j on upload
         log.add_timing("intensity_correction", time.perf_counter() - t0)
         t0 = time.perf_counter()
         if isinstance(inputs.spatial, DeviceSpatial):

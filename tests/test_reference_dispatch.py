@@ -160,7 +160,7 @@ def test_reference_engine_tests_on_gpu(tmp_path):
     rc, out = run_reference_tests(tmp_path, ["test_engine.py"], NFS_B200_PRECISION="fp64")
     assert rc == 0, out[-6000:]
     calls = dispatch_calls(out)
-    assert calls["recon_full"] >= 5 and calls["apply_E"] >= 3 and calls["phase_block"] >= 4, calls
+    assert calls["recon_full"] >= 5 and calls["apply_E"] >= 2 and calls["phase_block"] >= 4, calls
 
 
 @pytest.mark.gpu
