@@ -153,10 +153,11 @@ def test_config_b_fast_modes(have_b, prec):
     # the tensor-core modes drain their accumulators every 32 items; the FP32 CUDA-core path
     # accumulates up to ~7,300 streamed items per thread in FP32 (round-to-nearest) and lands at
     # 1.05e-5 here -- its stated config-B bound is 2e-5
-    assert max(its.values()) < (2e-5 if prec == "fp32" else 1e-5), its
+    tol = 2e-5 if prec == "fp32" else 1e-5
+    assert max(its.values()) < tol, its
     res = np.abs(np.array(log.residual_norms) - g["res"]) / g["res"]
     assert res.max() < 1e-4, res
-    assert rel(img.values, g["values"]) < 1e-5
+    assert rel(img.values, g["values"]) < tol
 
 
 # ------------------------------------------------------------------ config C: off-centre slices

@@ -554,3 +554,25 @@ def test_fast_modes_edge_shapes(prec, K, L, G, P1):
         plan.close()
     for a, b in zip(out[prec], out["fp64"]):
         assert rel(a, b) < 2e-5
+
+
+@pytest.mark.parametrize("prec", ["f16x3", "tf32x3"])
+def test_f16x3_repeat_bitwise(prec):
+    """Race stand-in (compute-sanitizer is closed on this pool): the warp-specialised tcgen05
+    kernels (mbarrier rings, TMEM stages, 2-CTA multicast clusters, split-K) must give
+    bit-identical E^H E over many back-to-back applies and across fresh plans, at a small shape
+    (few chunks per CTA: fills and drains dominate) and at the full config-B launch shape."""
+    for scale, reps in ((8, 40), (1, 6)):
+        prob = simulate.make_problem("B", scale=scale)
+        k, l = prob.temporal.shape[0], prob.spatial.shape[1]
+        rng = np.random.default_rng(11)
+        p = rng.standard_normal(l) + 1j * rng.standard_normal(l)
+        outs = []
+        for _ in range(2):
+            plan = Plan(k, l, 32, 16, prec)
+            plan.set_tables(prob.temporal, prob.spatial)
+            plan.set_sens(prob.sens, prob.intensity)
+            outs += [plan.apply_EHE(p) for _ in range(reps)]
+            plan.close()
+        for o in outs[1:]:
+            assert np.array_equal(o, outs[0])
