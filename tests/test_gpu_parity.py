@@ -205,7 +205,7 @@ def test_config_a_masked_with_filter_fp64():
                                  callback=lambda n, r: seen.__setitem__(n, r))
     assert rel(seen[5], g["rho_iters_mask"][0]) < 1e-12
     assert rel(seen[10], g["rho_iters_mask"][1]) < 1e-11
-    assert rel(img.values, g["values_mask"]) < 1e-3
+    assert rel(img.values, g["values_mask"]) < 1e-4   # measured 2.3e-5 (the CG is chaotic past it 11)
     labels = [lab for lab, _ in log.timings]
     assert labels[:3] == ["intensity_correction", "build_phase_matrix", "initial_adjoint"]
     assert labels[-2:] == ["apply_intensity", "apply_kfilter"]
