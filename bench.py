@@ -51,10 +51,14 @@ REF_PKG = os.path.join(ROOT, "baseline", "_ref")
 WORKLOADS = {
     "B": ("config B: 2D 256x256 single-shot spiral, L_R=41684 (disc mask), K=65536 samples "
           "(71.5 ms, R=4), 32 coils, B0 + 15 third-order field terms (P+1=16)"),
+    "C": ("config C: stack of 40 config-B slices (z = +-39 mm, 2 mm apart; third-order harmonics at each "
+          "slice's z), shared 65536-sample trajectory, 32 coils, P+1=16; slices are independent "
+          "replicas across ranks (no collective)"),
     "D": ("config D: 3D 128x128x64 stack of 64 spirals, L_R=532872 (ellipsoid mask), K=299648 samples "
           "(R~7), 32 coils, B0 + 15 third-order field terms (P+1=16)"),
 }
-ITERS = {"B": 20, "D": 50}
+ITERS = {"B": 20, "C": 20, "D": 50}
+N_SLICES = 40
 METRIC = "E^H E applies/s"
 FLUSH_BYTES = 256 << 20
 
@@ -161,7 +165,11 @@ def load_reference():
 
 
 def _problem(cfg):
+    """The configuration's problem; for C the most off-centre slice (z = +39 mm) stands for every
+    slice (all slices have the same sizes and per-pair cost)."""
     from paper_2604_09233_b200 import simulate
+    if cfg == "C":
+        return simulate.make_slices(N_SLICES, which=[N_SLICES - 1])[0]
     return simulate.make_problem(cfg)
 
 
@@ -227,7 +235,7 @@ def config_a_sigma(prob):
 def cpu_sample_rows(cfg):
     # ~10 s of CPU work per sample on an 8-32 core host: np.exp dominates (single-threaded,
     # ~35-57 ns per element)
-    return {"B": 3 * 402, "D": 256}[cfg]
+    return {"B": 3 * 402, "C": 3 * 402, "D": 256}[cfg]
 
 
 def run_reference_arm(args):
@@ -251,7 +259,7 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "applies/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak" if args.config == "C" else "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": bench_config(args.config),
         "cpu_baseline": {"value": value, "unit": "applies/s", "cores": _NCPU, "kind": kind,
@@ -267,6 +275,54 @@ def run_reference_arm(args):
 
 
 # ------------------------------------------------------------------ GPU arm
+def e2e_slices(args, engine, simulate, dist, world, rank, n_coils):
+    """Config C end to end: the 40-slice stack through engine.recon_slices (slice i on rank
+    i mod world, host arrays in and out); raw data of each slice synthesised once, outside the
+    timing, by the FP64 device forward operator."""
+    import torch
+    from paper_2604_09233_b200 import _native
+    slices = simulate.make_slices(N_SLICES)
+    inputs = []
+    for i, prob in enumerate(slices):
+        sigma = np.zeros((prob.temporal.shape[0], n_coils), np.complex128)
+        if i % world == rank:
+            pl = _native.Plan(prob.temporal.shape[0], prob.spatial.shape[1], n_coils, prob.spatial.shape[0], "fp64",
+                              int(os.environ.get("LOCAL_RANK", "0")))
+            pl.set_tables(prob.temporal, prob.spatial)
+            pl.set_sens(prob.sens)
+            sigma = pl.apply_E(prob.rho_true)
+            pl.close()
+        inputs.append(engine.EncodingInputs(sigma=sigma, spatial=prob.spatial, temporal=prob.temporal,
+                                            sens=prob.sens, intensity=prob.intensity, kfilter=None,
+                                            mask_r=prob.mask_r, grid=prob.grid, n_iter=ITERS["C"]))
+    times = []
+    for _ in range(args.e2e_steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        out = engine.recon_slices(inputs, precision=args.precision, gather=world > 1)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    e2e_s = min(times)
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    mine = [i for i in range(N_SLICES) if i % world == rank]
+    iters = sum(len(out[i][1].residual_norms) for i in mine) * world
+    per = inputs[0]
+    h2d = len(mine) * (per.temporal.nbytes + per.spatial.nbytes + per.sens.nbytes + per.intensity.nbytes
+                       + per.sigma.nbytes)
+    rel = [float(np.linalg.norm(out[i][0].values[p.mask_r] - p.rho_true) / np.linalg.norm(p.rho_true))
+           for i, p in zip(range(N_SLICES), slices) if out[i] is not None]
+    return {"value": iters / e2e_s, "unit": "applies/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(len(mine) * (per.spatial.shape[1] * 16 + 16 * ITERS["C"])),
+            "recon_seconds": e2e_s, "slices": N_SLICES, "cg_iterations": ITERS["C"],
+            "api": "paper_2604_09233_b200.recon_slices (host numpy in/out, slices as replicas)",
+            "rel_l2_vs_truth_max": max(rel) if rel else None}
+
+
 def roofline_for(args, kern_ms, k_loc, L, G, P1, clocks, sustained_peak=False):
     pk = peaks()
     flops_1 = float(k_loc) * L * (8 * G + 2 * P1)      # SURVEY 8d F1 per operator launch
@@ -317,7 +373,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default=os.environ.get("NFS_BENCH_CONFIG", "B"), choices=["B", "D"])
+    ap.add_argument("--config", default=os.environ.get("NFS_BENCH_CONFIG", "B"), choices=["B", "C", "D"])
     ap.add_argument("--precision", default=os.environ.get("NFS_BENCH_PRECISION", "f16x3"),
                     choices=["f16x3", "tf32x3", "fp32", "fp64"])
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -341,15 +397,16 @@ def main():
 
     from paper_2604_09233_b200 import _native, engine, simulate
 
-    prob = simulate.make_problem(args.config)
+    replicas = args.config == "C"   # slices: every rank runs whole, independent problems
+    prob = _problem(args.config)
     K, L = prob.temporal.shape[0], prob.spatial.shape[1]
     G, P1 = prob.sens.shape[1], prob.spatial.shape[0]
-    lo, hi = engine.shard_rows(K, rank, world)
+    lo, hi = (0, K) if replicas else engine.shard_rows(K, rank, world)
 
     plan = _native.Plan(hi - lo, L, G, P1, args.precision, local)
     stream = torch.cuda.Stream()
     plan.set_stream(stream.cuda_stream)
-    if world > 1:
+    if world > 1 and not replicas:
         plan.attach_comm(engine._nccl_unique_id(dist, rank), rank, world)
     plan.set_tables(prob.temporal[lo:hi], prob.spatial)
     plan.set_sens(prob.sens, prob.intensity)
@@ -394,7 +451,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = 1e3 / ms_per_step
+    value = 1e3 / ms_per_step * (world if replicas else 1)   # replicas: every rank applies its own
     kern_mean = [k / args.steps for k in kern_ms]
     roofline = roofline_for(args, kern_mean, hi - lo, L, G, P1, clocks)
     roofline["traffic"] = traffic_for(args, int(np.argmax(kern_mean)))
@@ -405,37 +462,44 @@ def main():
                                        sustained_peak=True)
 
     # end-to-end through the public API (host arrays in, image out)
-    inputs = engine.EncodingInputs(sigma=np.empty((K, G), np.complex128), spatial=prob.spatial,
-                                   temporal=prob.temporal, sens=prob.sens,
-                                   intensity=prob.intensity, kfilter=None, mask_r=prob.mask_r,
-                                   grid=prob.grid, n_iter=ITERS[args.config])
-    if world > 1:
-        full = [None] * world
-        dist.all_gather_object(full, sigma)
-        inputs.sigma = np.concatenate(full, 0)
+    if replicas:
+        e2e = e2e_slices(args, engine, simulate, dist, world, rank, G)
     else:
-        inputs.sigma = sigma
-    e2e_times = []
-    img = log = None
-    for _ in range(args.e2e_steps):
-        torch.cuda.synchronize()
+        inputs = engine.EncodingInputs(sigma=np.empty((K, G), np.complex128), spatial=prob.spatial,
+                                       temporal=prob.temporal, sens=prob.sens,
+                                       intensity=prob.intensity, kfilter=None, mask_r=prob.mask_r,
+                                       grid=prob.grid, n_iter=ITERS[args.config])
         if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        img, log = engine.recon_full(inputs, precision=args.precision)
-        torch.cuda.synchronize()
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_s = min(e2e_times)
-    if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    iters = len(log.residual_norms)
-    h2d = (prob.temporal.nbytes + prob.spatial.nbytes + prob.sens.nbytes + prob.intensity.nbytes
-           + inputs.sigma.nbytes)
-    d2h = L * 16 + 2 * 8 * iters
-    rel_truth = float(np.linalg.norm(img.values[prob.mask_r] - prob.rho_true)
-                      / np.linalg.norm(prob.rho_true))
+            full = [None] * world
+            dist.all_gather_object(full, sigma)
+            inputs.sigma = np.concatenate(full, 0)
+        else:
+            inputs.sigma = sigma
+        e2e_times = []
+        img = log = None
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            img, log = engine.recon_full(inputs, precision=args.precision)
+            torch.cuda.synchronize()
+            e2e_times.append(time.perf_counter() - t0)
+        e2e_s = min(e2e_times)
+        if world > 1:
+            t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        iters = len(log.residual_norms)
+        h2d = (prob.temporal.nbytes + prob.spatial.nbytes + prob.sens.nbytes + prob.intensity.nbytes
+               + inputs.sigma.nbytes)
+        d2h = L * 16 + 2 * 8 * iters
+        rel_truth = float(np.linalg.norm(img.values[prob.mask_r] - prob.rho_true)
+                          / np.linalg.norm(prob.rho_true))
+        e2e = {"value": iters / e2e_s, "unit": "applies/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "recon_seconds": e2e_s, "cg_iterations": iters,
+               "api": "paper_2604_09233_b200.recon_full (host numpy in/out)",
+               "rel_l2_vs_truth": rel_truth}
 
     # config A through the public API, next to the reference arm's fully timed config-A solve
     cfg_a = None
@@ -471,21 +535,19 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "weak" if replicas else "strong", "vs_baseline": None,
             "dtype": {"fp32": "fp32", "fp64": "fp64", "tf32x3": "tf32x3 (fp32 accumulate)",
                       "f16x3": "f16x3 split contraction (exact int8 phase, fp32 accumulate)"}[args.precision],
             "data": "synthetic (disc phantom, synthetic coils, linear B0; raw data from the device forward model)",
             "config": bench_config(args.config),
             "precision": args.precision,
-            "parallelism": f"sample-sharded x{world}" if world > 1 else "1 GPU",
+            "parallelism": (f"slice replicas x{world}" if replicas else f"sample-sharded x{world}")
+                           if world > 1 else "1 GPU",
             "plan": plan.describe(),
             "roofline": roofline,
             "sustained": sus,
             "cpu_baseline": cpu,
-            "e2e": {"value": iters / e2e_s, "unit": "applies/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "recon_seconds": e2e_s, "cg_iterations": iters,
-                    "api": "paper_2604_09233_b200.recon_full (host numpy in/out)",
-                    "rel_l2_vs_truth": rel_truth},
+            "e2e": e2e,
             "config_a_recon": cfg_a,
             "clocks": clocks,
             "gpu_launches": launches * args.steps,
