@@ -127,8 +127,8 @@ __global__ void __launch_bounds__(512, 1) k(int iters, uint32_t* out, long long*
 }
 int main() {
   uint32_t* o; long long* c; cudaMalloc(&o, 148 * 2048 * 4); cudaMallocManaged(&c, 8);
-  for (int mode = 2; mode < 9; ++mode)
-  for (int w = 4; w <= 16; w *= 2) {
+  for (int mode = 0; mode < 9; ++mode)
+  for (int w : {4, 8, 12, 16}) {
     const int iters = 500;
     if (mode == 0) k<32, 0><<<148, w * 32>>>(iters, o, c);
     if (mode == 1) k<32, 1><<<148, w * 32>>>(iters, o, c);
