@@ -66,6 +66,12 @@ int nfs_plan_set_stream(nfs_plan* plan, void* stream);
  * image is all-reduced (sum) once per CG iteration.  world == 1 needs no call (a 1-rank
  * communicator is accepted and exercises the same all-reduce path). */
 int nfs_plan_attach_comm(nfs_plan* plan, const void* nccl_unique_id, int32_t rank, int32_t world);
+/* A communicator shared by all plans of a process (created once per rank, borrowed by every
+ * plan with nfs_plan_use_comm and destroyed by nfs_comm_destroy after the last plan), so
+ * repeated reconstructions do not pay ncclCommInitRank each time. */
+int nfs_comm_create(const void* nccl_unique_id, int32_t rank, int32_t world, int32_t device, void** comm);
+void nfs_comm_destroy(void* comm);
+int nfs_plan_use_comm(nfs_plan* plan, void* comm, int32_t rank, int32_t world);
 
 /* Basis tables: temporal rows of this rank (K x P1) and spatial (P1 x L_R). */
 int nfs_set_tables(nfs_plan* plan, const double* temporal, const double* spatial);

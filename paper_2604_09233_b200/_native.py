@@ -37,6 +37,9 @@ SIGNATURES = {
     "nfs_plan_destroy": (None, [_c_void_p]),
     "nfs_plan_set_stream": (_c_i32, [_c_void_p, _c_void_p]),
     "nfs_plan_attach_comm": (_c_i32, [_c_void_p, ctypes.c_char_p, _c_i32, _c_i32]),
+    "nfs_comm_create": (_c_i32, [ctypes.c_char_p, _c_i32, _c_i32, _c_i32, ctypes.POINTER(_c_void_p)]),
+    "nfs_comm_destroy": (None, [_c_void_p]),
+    "nfs_plan_use_comm": (_c_i32, [_c_void_p, _c_void_p, _c_i32, _c_i32]),
     "nfs_set_tables": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
     "nfs_set_tables_t": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
     "nfs_set_tables_grid": (_c_i32, [_c_void_p, _c_dbl_p, ctypes.POINTER(_c_i64), _c_dbl_p,
@@ -149,6 +152,9 @@ class Plan:
 
     def attach_comm(self, unique_id: bytes, rank: int, world: int):
         _check(self._lib.nfs_plan_attach_comm(self._h, unique_id, rank, world))
+
+    def use_comm(self, comm: "SharedComm"):
+        _check(self._lib.nfs_plan_use_comm(self._h, comm.handle, comm.rank, comm.world))
 
     # -- inputs ------------------------------------------------------------------
     def set_tables(self, temporal, spatial):
@@ -328,3 +334,18 @@ def intensity_correction(sens_full, vox_index, device: int = 0) -> np.ndarray:
                                         int(full.shape[1]), idx.ctypes.data_as(ctypes.POINTER(_c_i64)),
                                         int(idx.size), _dp(out)))
     return out
+
+
+class SharedComm:
+    """One NCCL communicator per rank, shared by every plan of the process (nfs_comm_create)."""
+
+    def __init__(self, unique_id: bytes, rank: int, world: int, device: int):
+        lib = load_library()
+        h = _c_void_p()
+        _check(lib.nfs_comm_create(unique_id, int(rank), int(world), int(device), ctypes.byref(h)))
+        self._lib, self.handle, self.rank, self.world, self.device = lib, h, int(rank), int(world), int(device)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.nfs_comm_destroy(self.handle)
+            self.handle = None

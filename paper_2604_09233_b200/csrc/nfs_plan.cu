@@ -107,6 +107,7 @@ struct nfs_plan {
   int split_f = 1, split_a = 1;
   bool have_tables = false, have_sens = false, have_samples = false;
   nfsNcclComm comm = nullptr;
+  bool owns_comm = true;   // false: a shared communicator (nfs_plan_use_comm) outlives the plan
   int rank = 0, world = 1;
   nfs::TcPlan* tc = nullptr;            // tensor-core operator, FP32 phase (NFS_PREC_TF32X3)
   nfs::TciPlan* tci = nullptr;          // tensor-core operator, exact int8 phase (NFS_PREC_F16X3)
@@ -297,7 +298,7 @@ extern "C" void nfs_plan_destroy(nfs_plan* P) {
                   P->d_ssim_sel};
   for (void* b : bufs)
     if (b) nfs::dev_free(b);
-  if (P->comm && nccl_api().ok) nccl_api().destroy(P->comm);
+  if (P->comm && P->owns_comm && nccl_api().ok) nccl_api().destroy(P->comm);
   if (P->own_stream && P->stream) cudaStreamDestroy(P->stream);
   delete P;
 }
@@ -330,6 +331,39 @@ extern "C" int nfs_plan_attach_comm(nfs_plan* P, const void* uid, int32_t rank, 
   int n = -1;
   if (api.count) api.count(P->comm, &n);   // the communicator's own rank count, for the logs
   P->desc += " [nccl comm rank " + std::to_string(rank) + " of " + std::to_string(n) + "]";
+  return NFS_OK;
+}
+
+// A communicator shared by every plan of a process (one per rank, created once): plans borrow
+// it with nfs_plan_use_comm, so a recon does not pay ncclCommInitRank again.
+extern "C" int nfs_comm_create(const void* uid, int32_t rank, int32_t world, int32_t device, void** comm) {
+  if (!uid || !comm || world < 1 || rank < 0 || rank >= world) return fail(NFS_ERR_INVALID, "bad rank/world");
+  NcclApi& api = nccl_api();
+  if (!api.ok) return fail(NFS_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  NFS_CUDA(cudaSetDevice(device));
+  nfsNcclUniqueId id;
+  memcpy(id.internal, uid, 128);
+  nfsNcclComm c = nullptr;
+  int r = api.init_rank(&c, world, id, rank);
+  if (r != 0) return fail(NFS_ERR_NCCL, std::string("ncclCommInitRank: ") + (api.errstr ? api.errstr(r) : "?"));
+  *comm = c;
+  return NFS_OK;
+}
+
+extern "C" void nfs_comm_destroy(void* comm) {
+  if (comm && nccl_api().ok) nccl_api().destroy((nfsNcclComm)comm);
+}
+
+extern "C" int nfs_plan_use_comm(nfs_plan* P, void* comm, int32_t rank, int32_t world) {
+  if (!P || !comm || world < 1 || rank < 0 || rank >= world) return fail(NFS_ERR_INVALID, "bad communicator");
+  if (P->comm && P->owns_comm && nccl_api().ok) nccl_api().destroy(P->comm);
+  P->comm = (nfsNcclComm)comm;
+  P->owns_comm = false;
+  P->rank = rank;
+  P->world = world;
+  int n = -1;
+  if (nccl_api().count) nccl_api().count(P->comm, &n);
+  P->desc += " [shared nccl comm rank " + std::to_string(rank) + " of " + std::to_string(n) + "]";
   return NFS_OK;
 }
 

@@ -422,6 +422,20 @@ def _nccl_unique_id(dist, rank):
     return obj[0]
 
 
+_COMMS = {}
+
+
+def _shared_comm(dist, rank, world, device):
+    """The process's NCCL communicator for (rank, world, device): created once (one unique-id
+    broadcast), then borrowed by every plan, so repeated recons skip ncclCommInitRank."""
+    key = (rank, world, device)
+    comm = _COMMS.get(key)
+    if comm is None:
+        comm = _native.SharedComm(_nccl_unique_id(dist, rank), rank, world, device)
+        _COMMS[key] = comm
+    return comm
+
+
 def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label: bool, shard: bool = True):
     """Create the device plan for this rank's sample shard; upload tables, S', sigma.
 
@@ -434,7 +448,7 @@ def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label:
                         inputs.spatial.shape[0], precision, device)
     try:
         if world > 1:
-            plan.attach_comm(_nccl_unique_id(dist, rank), rank, world)
+            plan.use_comm(_shared_comm(dist, rank, world, device))
         t_plan = time.perf_counter() - t0
         t0 = time.perf_counter()
         if isinstance(inputs.sens, DeviceSens):              # restriction + S' = S o j on the GPU

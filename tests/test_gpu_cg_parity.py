@@ -204,3 +204,22 @@ def test_config_c_stack_replicas_full_size():
         assert log.residual_norms[-1] < 0.1 * log.residual_norms[0]
     ref, _ = engine.recon_full(inputs[-1], precision="fp64")
     assert rel(out[-1][0].values, ref.values) < 1e-5
+
+
+def test_config_d_full_size_f16x3_tracks_fp64():
+    """Config D at FULL size on the production launch shape (L_R = 532,872, K = 299,648, 32 coils,
+    P+1 = 16): the first CG iterations of the f16x3 solve track the FP64 device solve (whose
+    operator is pinned to the reference at the scaled 3D shape and on row subsets here) within the
+    fast-mode bound.  The CPU reference needs ~85 min per iteration at this size."""
+    prob = simulate.make_problem("D")
+    sigma = _device_sigma(prob, prob.rho_true)
+    mk = lambda: engine.EncodingInputs(  # noqa: E731
+        sigma=sigma, spatial=prob.spatial, temporal=prob.temporal, sens=prob.sens,
+        intensity=prob.intensity, kfilter=None, mask_r=prob.mask_r, grid=prob.grid, n_iter=3)
+    seen = {}
+    ref, lref = engine.recon_full(mk(), precision="fp64", callback=lambda n, r: seen.__setitem__(("fp64", n), r))
+    img, log = engine.recon_full(mk(), precision="f16x3", callback=lambda n, r: seen.__setitem__(("f16x3", n), r))
+    for n in (1, 2, 3):
+        assert rel(seen[("f16x3", n)], seen[("fp64", n)]) < 1e-5, n
+    res = np.abs(np.array(log.residual_norms) - lref.residual_norms) / np.array(lref.residual_norms)
+    assert res.max() < 1e-4

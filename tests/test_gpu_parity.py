@@ -304,6 +304,29 @@ def test_nccl_allreduce_path_single_rank():
     assert rel(res[1], g["full_values"]) < 1e-10
 
 
+def test_shared_communicator_reused_across_plans():
+    """One NCCL communicator per rank (nfs_comm_create) borrowed by successive plans, as the
+    engine does for repeated sharded recons: results unchanged, the communicator survives the
+    plans that used it."""
+    import torch.cuda.nccl as tnccl
+    from paper_2604_09233_b200._native import SharedComm
+    g = golden("engine8")
+    comm = SharedComm(bytes(tnccl.unique_id()), 0, 1, 0)
+    outs = []
+    for _ in range(3):
+        plan = Plan(90, 64, 3, 3, "fp64")
+        plan.use_comm(comm)
+        assert "shared nccl comm rank 0 of 1" in plan.describe()
+        plan.set_tables(g["temporal"], g["spatial"])
+        plan.set_sens(g["sens"])
+        plan.set_samples(g["sigma"])
+        outs.append(plan.cg_solve(15)[0])
+        plan.close()
+    comm.close()
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    assert rel(outs[0], g["full_values"]) < 1e-10
+
+
 # ------------------------------------------------------------------ config D (f2: device synthesis)
 @pytest.fixture(scope="module")
 def problem_d():
