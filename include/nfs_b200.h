@@ -100,6 +100,11 @@ int nfs_intensity_correction(int32_t device, const double* sens_full, int64_t n_
                              const int64_t* vox_index, int64_t n_r, double* j_out);
 /* Raw samples of this rank (K x G complex); non-finite -> NFS_ERR_NONFINITE. */
 int nfs_set_samples(nfs_plan* plan, const double* sigma);
+/* Samples read straight from a dataset file: rows [row0, row0 + n_samples) of a
+ * raw little-endian complex128 (K_total, n_coils) array -- the reference's `sigma.c128`
+ * (nfs/core.py:292-328) -- through the pinned staging ring; a sharded rank reads only its rows.
+ * Same finiteness check as nfs_set_samples; NFS_ERR_INVALID on a short read. */
+int nfs_set_samples_file(nfs_plan* plan, const char* path, int64_t row0);
 
 /* Per-iteration diagnostic on the device: relative RMSE of the image rho o j vs
  * a reference (nfs/metrics.py:73-88 as called from a convergence-study callback) is logged by

@@ -8,6 +8,7 @@ and signatures, backed by hand-written sm_100a CUDA kernels behind a C ABI
 from .core import Grid, ReconImage, grid_coordinates
 from .engine import (
     CGLog,
+    DatasetSamples,
     DeviceRMSE,
     DeviceSens,
     DeviceSSIM,
@@ -27,7 +28,7 @@ from .engine import (
 )
 
 __all__ = [
-    "CGLog", "DeviceRMSE", "DeviceSens", "DeviceSSIM", "DeviceSpatial", "EncodingInputs", "EngineError", "Grid", "MemoryBudgetError", "ReconImage",
+    "CGLog", "DatasetSamples", "DeviceRMSE", "DeviceSens", "DeviceSSIM", "DeviceSpatial", "EncodingInputs", "EngineError", "Grid", "MemoryBudgetError", "ReconImage",
     "apply_E", "apply_EH", "build_bases", "choose_block_starts", "grid_coordinates", "intensity_correction",
     "phase_block", "recon_full", "recon_slices", "recon_split",
 ]

@@ -49,6 +49,7 @@ SIGNATURES = {
     "nfs_intensity_correction": (_c_i32, [_c_i32, _c_dbl_p, _c_i64, _c_i32, ctypes.POINTER(_c_i64), _c_i64,
                                           _c_dbl_p]),
     "nfs_set_samples": (_c_i32, [_c_void_p, _c_dbl_p]),
+    "nfs_set_samples_file": (_c_i32, [_c_void_p, ctypes.c_char_p, _c_i64]),
     "nfs_apply_E": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
     "nfs_apply_EH": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
     "nfs_apply_EHE": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
@@ -201,6 +202,10 @@ class Plan:
                                            idx.ctypes.data_as(ctypes.POINTER(_c_i64)),
                                            None if jin is None else _dp(jin), _dp(j_out)))
         return j_out
+
+    def set_samples_file(self, path: str, row0: int = 0):
+        """Samples = rows [row0, row0 + n_samples) of a raw complex128 (K, coils) dataset file."""
+        _check(self._lib.nfs_set_samples_file(self._h, os.fsencode(path), int(row0)))
 
     def set_samples(self, sigma):
         k, _, g, _ = self.shape

@@ -76,6 +76,7 @@ inline void dev_free(void* p) {
 // Host -> device copy of a caller (pageable) array through a pinned staging ring with
 // multi-threaded staging (nfs_upload.cu); same semantics as cudaMemcpyAsync from pageable memory.
 cudaError_t h2d(void* dst, const void* src, size_t bytes, cudaStream_t st);
+cudaError_t h2d_file(void* dst, const char* path, int64_t offset, size_t bytes, cudaStream_t st);
 
 template <typename T> struct C2;
 template <> struct C2<float> { using type = float2; };

@@ -605,12 +605,33 @@ static int upload_samples(nfs_plan* P, const double* sigma, void* dst) {
   return NFS_OK;
 }
 
+static int finish_samples(nfs_plan* P);
+
 extern "C" int nfs_set_samples(nfs_plan* P, const double* sigma) {
   if (!P || (!sigma && P->K > 0)) return fail(NFS_ERR_INVALID, "null samples");
   NFS_CUDA(cudaSetDevice(P->device));
   const size_t n = (size_t)P->K * P->G;
   NFS_TRY(ensure_io(P, std::max<size_t>(n, (size_t)P->L)));
   NFS_CUDA(nfs::h2d(P->d_io, sigma, n * sizeof(double2), P->stream));
+  return finish_samples(P);
+}
+
+// Samples straight from a dataset file: rows [row0, row0 + K) of a raw little-endian complex128
+// (K_total, n_coils) array (the reference's `sigma.c128`, nfs/core.py:292-328) -- a sharded rank
+// reads only its own rows from disk.
+extern "C" int nfs_set_samples_file(nfs_plan* P, const char* path, int64_t row0) {
+  if (!P || !path || row0 < 0) return fail(NFS_ERR_INVALID, "bad sample file arguments");
+  NFS_CUDA(cudaSetDevice(P->device));
+  const size_t n = (size_t)P->K * P->G;
+  NFS_TRY(ensure_io(P, std::max<size_t>(n, (size_t)P->L)));
+  const cudaError_t e = nfs::h2d_file(P->d_io, path, row0 * (int64_t)P->G * 16, n * sizeof(double2), P->stream);
+  if (e == cudaErrorInvalidValue) return fail(NFS_ERR_INVALID, std::string("cannot read the sample rows from ") + path);
+  NFS_CUDA(e);
+  return finish_samples(P);
+}
+
+static int finish_samples(nfs_plan* P) {
+  const size_t n = (size_t)P->K * P->G;
   unsigned int bad = 0;
   unsigned int* d_bad = reinterpret_cast<unsigned int*>(P->d_partials);   // reduction scratch
   NFS_CUDA(nfs::launch_count_nonfinite(reinterpret_cast<const double*>(P->d_io), (int64_t)n * 2, d_bad, P->stream));

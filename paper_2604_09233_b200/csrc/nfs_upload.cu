@@ -7,8 +7,10 @@
 // staged: config B's 69 MB of tables, coil maps and samples upload in ≈2 ms instead of ≈6.5.
 // Semantics match cudaMemcpyAsync from pageable memory: the source may be reused as soon as the
 // call returns, the destination is valid in stream order on `st`.
+#include <fcntl.h>
 #include <omp.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <mutex>
@@ -76,6 +78,53 @@ cudaError_t h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if ((e = cudaEventRecord(s.done[k], st)) != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// Same, with the source a byte range of a file (the reference's raw dataset arrays, nfs/core.py
+// Dataset: little-endian binary, complex as interleaved (re, im)): each staging slot is filled
+// by several threads' pread()s, so a rank reads ONLY its own range from disk straight into the
+// pinned ring -- no host array of the whole dataset.  Returns cudaErrorInvalidValue on a short
+// read or an unreadable file.
+cudaError_t h2d_file(void* dst, const char* path, int64_t offset, size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return cudaErrorInvalidValue;
+  std::lock_guard<std::mutex> lock(g_mu);
+  if (dev < 0 || dev >= 64 || !stage_init(g_stage[dev])) {
+    close(fd);
+    return cudaErrorMemoryAllocation;
+  }
+  Stage& s = g_stage[dev];
+  unsigned char* out = static_cast<unsigned char*>(dst);
+  static int next[64] = {};
+  bool short_read = false;
+  for (size_t off = 0; off < bytes && !short_read; off += SLOT_BYTES) {
+    const size_t n = std::min(SLOT_BYTES, bytes - off);
+    const int k = next[dev];
+    next[dev] = (k + 1) % N_SLOTS;
+    if ((e = cudaEventSynchronize(s.done[k])) != cudaSuccess) break;
+    const int nt = std::max(1, std::min(8, omp_get_num_procs() / 2));
+    const size_t per = (n + nt - 1) / nt;
+    int bad = 0;
+#pragma omp parallel for num_threads(nt) schedule(static) reduction(+ : bad)
+    for (int t = 0; t < nt; ++t) {
+      size_t a = std::min(n, (size_t)t * per);
+      const size_t b = std::min(n, a + per);
+      while (a < b) {
+        const ssize_t r = pread(fd, s.slot[k] + a, b - a, (off_t)(offset + off + a));
+        if (r <= 0) { ++bad; break; }
+        a += (size_t)r;
+      }
+    }
+    if (bad) { short_read = true; break; }
+    if ((e = cudaMemcpyAsync(out + off, s.slot[k], n, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+    if ((e = cudaEventRecord(s.done[k], st)) != cudaSuccess) break;
+  }
+  close(fd);
+  if (e != cudaSuccess) return e;
+  return short_read ? cudaErrorInvalidValue : cudaSuccess;
 }
 
 }  // namespace nfs

@@ -30,7 +30,7 @@ from .simulate import solid_harmonics
 __all__ = [
     "EngineError", "MemoryBudgetError", "EncodingInputs", "CGLog", "phase_block", "apply_E",
     "apply_EH", "recon_full", "recon_split", "choose_block_starts", "build_bases",
-    "default_precision", "PhaseBlock", "DeviceSens", "intensity_correction",
+    "default_precision", "PhaseBlock", "DeviceSens", "DatasetSamples", "intensity_correction",
 ]
 
 
@@ -337,6 +337,48 @@ class DeviceSens:
         return self._j
 
 
+class DatasetSamples:
+    """The raw coil samples of a reference dataset directory, left on disk: the
+    reference stores them as `sigma.c128`, raw little-endian complex128 (K, coils) listed in
+    `manifest.json` (nfs/core.py:292-328).  Used as EncodingInputs.sigma, each rank's plan reads
+    ONLY its own sample rows from the file through the pinned staging ring
+    (`nfs_set_samples_file`); `np.asarray(handle)` loads the whole array like
+    `Dataset.load_array`.  Accepts a dataset directory or an nfsense `Dataset`."""
+
+    __array_priority__ = 10
+
+    def __init__(self, dataset, name: str = "sigma"):
+        import json
+        root = getattr(dataset, "path", dataset)
+        root = os.fspath(root)
+        with open(os.path.join(root, "manifest.json"), encoding="utf-8") as fh:
+            entry = json.load(fh).get("arrays", {}).get(name)
+        if entry is None:
+            raise EngineError(f"dataset has no array {name!r}")
+        if entry["dtype"] != "c128" or len(entry["shape"]) != 2:
+            raise EngineError(f"array {name!r} is not a (samples, coils) complex128 array")
+        self.path = os.path.join(root, entry["file"])
+        self._shape = (int(entry["shape"][0]), int(entry["shape"][1]))
+        if os.path.getsize(self.path) != self._shape[0] * self._shape[1] * 16:
+            raise EngineError(f"array {name!r}: file size does not match its shape")
+
+    @property
+    def shape(self):
+        return self._shape
+
+    @property
+    def ndim(self):
+        return 2
+
+    @property
+    def dtype(self):
+        return np.dtype(np.complex128)
+
+    def __array__(self, dtype=None, copy=None):
+        out = np.fromfile(self.path, dtype="<c16").reshape(self._shape)
+        return out if dtype is None else out.astype(dtype)
+
+
 def intensity_correction(maps: np.ndarray, mask_r) -> np.ndarray:
     """nfs/sensmaps.py:145-152 on the GPU: j = 1/sqrt(sum_coils |S|^2) on the mask, else 0."""
     mask_r = np.asarray(mask_r, dtype=bool).reshape(-1)
@@ -436,6 +478,25 @@ def _shared_comm(dist, rank, world, device):
     return comm
 
 
+def _upload_agreed(dist, upload):
+    """Run `upload` (a per-rank check happens inside); with several ranks, every rank learns
+    whether any rank failed before the first collective of the solve, so none is left blocked."""
+    err = None
+    try:
+        upload()
+    except EngineError as exc:
+        err = exc
+    if dist is not None:
+        import torch
+        flag = torch.tensor([0 if err is None else 1], dtype=torch.int32,
+                            device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(flag)
+        if err is None and int(flag.item()) > 0:
+            err = EngineError("raw data contains non-finite values (on another rank)")
+    if err is not None:
+        raise err
+
+
 def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label: bool, shard: bool = True):
     """Create the device plan for this rank's sample shard; upload tables, S', sigma.
 
@@ -463,7 +524,10 @@ def _make_plan(inputs: EncodingInputs, precision: str, log: CGLog, timing_label:
             plan.set_tables(inputs.temporal[lo:hi], inputs.spatial)
         if timing_label:   # the GPU analogue of building P: plan + table upload
             log.add_timing("build_phase_matrix", t_plan + time.perf_counter() - t0)
-        plan.set_samples(inputs.sigma[lo:hi])   # raw data finiteness checked on the device
+        if isinstance(inputs.sigma, DatasetSamples):   # this rank's rows straight from the file
+            _upload_agreed(dist if world > 1 else None, lambda: plan.set_samples_file(inputs.sigma.path, lo))
+        else:
+            plan.set_samples(inputs.sigma[lo:hi])   # raw data finiteness checked on the device
     except BaseException:
         plan.close()
         raise
@@ -530,6 +594,8 @@ def recon_full(inputs: EncodingInputs, memory_budget_bytes: int | None = None, c
 def _check_samples(inputs: EncodingInputs, shard: bool):
     # single rank: nfs_set_samples checks finiteness on the device (same error); sharded: every
     # rank must fail together before any collective, so check the full array on the host
+    if isinstance(inputs.sigma, DatasetSamples):   # checked per rank on upload (_upload_agreed)
+        return
     if shard and _dist_info()[2] > 1 and not np.all(np.isfinite(inputs.sigma)):
         raise EngineError("raw data contains non-finite values")
 

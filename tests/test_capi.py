@@ -143,3 +143,21 @@ def test_header_is_plain_c_and_links(tmp_path):
                     lib_path, "-o", str(exe), f"-Wl,-rpath,{os.path.dirname(lib_path)}"], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
     assert out.strip()
+
+
+def test_dataset_samples_handle_host_side(tmp_path):
+    """engine.DatasetSamples reads the reference's dataset manifest (nfs/core.py:292-328) and
+    loads the whole array like Dataset.load_array when materialised (no GPU needed)."""
+    import json
+    from paper_2604_09233_b200 import engine
+    sig = (np.arange(12) + 1j * np.arange(12)[::-1]).reshape(6, 2)
+    sig.astype("<c16").tofile(tmp_path / "sigma.c128")
+    (tmp_path / "manifest.json").write_text(json.dumps(
+        {"version": 1, "arrays": {"sigma": {"file": "sigma.c128", "dtype": "c128", "shape": [6, 2]}}}))
+    h = engine.DatasetSamples(tmp_path)
+    assert h.shape == (6, 2) and h.ndim == 2
+    assert np.array_equal(np.asarray(h), sig)
+    (tmp_path / "manifest.json").write_text(json.dumps(
+        {"version": 1, "arrays": {"sigma": {"file": "sigma.c128", "dtype": "c128", "shape": [7, 2]}}}))
+    with pytest.raises(engine.EngineError):
+        engine.DatasetSamples(tmp_path)

@@ -65,3 +65,60 @@ def test_voxel_index_outside_grid_rejected():
     with pytest.raises(engine.EngineError):
         bad.intensity
     assert grid_coordinates(pm.grid).shape[0] == pm.grid.nvox
+
+
+def _write_dataset(tmp_path, sigma):
+    """A dataset directory in the reference's on-disk format (nfs/core.py:292-328): raw
+    little-endian complex128 + manifest.json."""
+    import json
+    np.ascontiguousarray(sigma, dtype="<c16").tofile(tmp_path / "sigma.c128")
+    (tmp_path / "manifest.json").write_text(json.dumps(
+        {"version": 1, "grid": {"dims": [64, 64, 1], "fov_m": [0.22, 0.22, 0.002]}, "counts": {},
+         "echo_times_s": [], "byte_order": "little", "element_order": "x-fastest",
+         "arrays": {"sigma": {"file": "sigma.c128", "dtype": "c128", "shape": list(sigma.shape)}}}))
+    return tmp_path
+
+
+@pytest.mark.parametrize("prec", ["fp64", "f16x3"])
+def test_samples_read_from_dataset_file(tmp_path, prec):
+    """the raw samples go from the dataset file to the device through the pinned
+    ring (nfs_set_samples_file) -- same reconstruction, bit for bit, as from a host array."""
+    g = golden("config_a")
+    pm = simulate.make_problem("A_mask")
+    ds = engine.DatasetSamples(_write_dataset(tmp_path, g["sigma"]))
+    assert ds.shape == g["sigma"].shape and np.array_equal(np.asarray(ds), g["sigma"])
+    mk = lambda sig: engine.EncodingInputs(  # noqa: E731
+        sigma=sig, spatial=pm.spatial, temporal=pm.temporal, sens=pm.sens, intensity=pm.intensity,
+        kfilter=None, mask_r=pm.mask_r, grid=pm.grid, n_iter=8)
+    a, la = engine.recon_full(mk(g["sigma"]), precision=prec)
+    b, lb = engine.recon_full(mk(ds), precision=prec)
+    assert np.array_equal(a.values, b.values) and la.residual_norms == lb.residual_norms
+
+
+def test_sample_rows_of_a_shard_from_file(tmp_path):
+    """A sharded rank reads only rows [lo, hi) of the file: the shard plan's adjoint equals the
+    one fed with the same rows from memory."""
+    from paper_2604_09233_b200._native import Plan
+    g = golden("config_a")
+    pm = simulate.make_problem("A_mask")
+    path = _write_dataset(tmp_path, g["sigma"]) / "sigma.c128"
+    k = pm.temporal.shape[0]
+    lo, hi = engine.shard_rows(k, 1, 3)
+    outs = []
+    for from_file in (False, True):
+        plan = Plan(hi - lo, pm.spatial.shape[1], 8, 3, "fp64")
+        plan.set_tables(pm.temporal[lo:hi], pm.spatial)
+        plan.set_sens(pm.sens, pm.intensity)
+        if from_file:
+            plan.set_samples_file(str(path), lo)
+        else:
+            plan.set_samples(g["sigma"][lo:hi])
+        outs.append(plan.cg_solve(3)[0])
+        plan.close()
+    assert np.array_equal(outs[0], outs[1])
+    bad = Plan(hi - lo, pm.spatial.shape[1], 8, 3, "fp64")
+    bad.set_tables(pm.temporal[lo:hi], pm.spatial)
+    bad.set_sens(pm.sens, pm.intensity)
+    with pytest.raises(engine.EngineError):
+        bad.set_samples_file(str(path), k - 10)          # runs past the end of the file
+    bad.close()
