@@ -73,15 +73,14 @@ __global__ void to_float_kernel(const double* __restrict__ in, float* __restrict
 
 // temporal [K][P1] (rad) -> tt [K][nt] (turns, zero padded); spatial [P1][L] -> rr [L][nt]
 __global__ void prep_tables_kernel(const double* __restrict__ temporal, const double* __restrict__ spatial,
-                                   int64_t K, int64_t L, int p1, int nt, bool spatial_lp,
+                                   int64_t K, int64_t L, int p1, int nt, bool spatial_lp, double tscale,
                                    double* __restrict__ tt, double* __restrict__ rr) {
-  const double inv2pi = 1.0 / 6.283185307179586476925286766559;
   const int64_t nk = K * nt, total = nk + L * nt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < nk) {
       const int64_t k = i / nt;
       const int p = (int)(i - k * nt);
-      tt[i] = p < p1 ? temporal[k * p1 + p] * inv2pi : 0.0;
+      tt[i] = p < p1 ? temporal[k * p1 + p] * tscale : 0.0;
     } else {
       const int64_t j = i - nk, l = j / nt;
       const int p = (int)(j - l * nt);
@@ -201,10 +200,14 @@ cudaError_t launch_to_float(const double* d_in, float* d_out, int64_t n, cudaStr
   return cudaGetLastError();
 }
 
+// temporal table in turns (temporal / 2pi: the FP32 and tensor-core paths) or, radians = true, as
+// given (the FP64 parity path computes phi = temporal . spatial exactly like the reference's dgemm
+// and takes sin/cos of phi itself)
 cudaError_t launch_prep_tables(const double* d_temporal, const double* d_spatial, int64_t K, int64_t L, int p1,
-                               int nt, double* d_tt, double* d_rr, cudaStream_t st, bool spatial_lp) {
-  prep_tables_kernel<<<grid_for((K + L) * nt), 256, 0, st>>>(d_temporal, d_spatial, K, L, p1, nt, spatial_lp, d_tt,
-                                                             d_rr);
+                               int nt, double* d_tt, double* d_rr, cudaStream_t st, bool spatial_lp, bool radians) {
+  const double tscale = radians ? 1.0 : 1.0 / 6.283185307179586476925286766559;
+  prep_tables_kernel<<<grid_for((K + L) * nt), 256, 0, st>>>(d_temporal, d_spatial, K, L, p1, nt, spatial_lp, tscale,
+                                                             d_tt, d_rr);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,7 @@ cudaError_t launch_col_absmax(const double* d_tab, int64_t n, int nt, unsigned l
 cudaError_t launch_to_float(const double* d_in, float* d_out, int64_t n, cudaStream_t st);
 cudaError_t launch_prep_tables(const double* d_temporal, const double* d_spatial, int64_t K, int64_t L, int p1,
                                int nt, double* d_tt, double* d_rr, cudaStream_t st,
-                               bool spatial_lp = false);
+                               bool spatial_lp = false, bool radians = false);
 cudaError_t launch_prep_sens(const double2* d_sens, const double* d_j, int64_t L, int g, int ldc, bool fp64,
                              void* d_out, cudaStream_t st);
 cudaError_t launch_intensity(const double2* d_full, const int64_t* d_idx, int64_t n_r, int g, double* d_j,

@@ -463,7 +463,8 @@ static int set_tables_impl(nfs_plan* P, const double* temporal, const double* sp
   NFS_CUDA(sc.get(&d_rr, (size_t)L * nt * 8));
   if (K > 0) NFS_CUDA(nfs::h2d(d_temp, temporal, (size_t)K * p1 * 8, P->stream));
   NFS_CUDA(nfs::h2d(d_spat, spatial, (size_t)p1 * L * 8, P->stream));
-  NFS_CUDA(nfs::launch_prep_tables(d_temp, d_spat, K, L, p1, nt, d_tt, d_rr, P->stream, spatial_lp));
+  NFS_CUDA(nfs::launch_prep_tables(d_temp, d_spat, K, L, p1, nt, d_tt, d_rr, P->stream, spatial_lp,
+                                   P->prec == NFS_PREC_FP64));
   return finish_tables(P, d_tt, d_rr);
 }
 
@@ -506,7 +507,8 @@ extern "C" int nfs_set_tables_grid(nfs_plan* P, const double* temporal, const in
   NFS_CUDA(cudaMemcpyAsync(d_vox, vox_index, L * 8, cudaMemcpyHostToDevice, P->stream));
   NFS_CUDA(cudaMemcpyAsync(d_b0, b0_masked, L * 8, cudaMemcpyHostToDevice, P->stream));
   if (K > 0) NFS_CUDA(nfs::h2d(d_temp, temporal, (size_t)K * p1 * 8, P->stream));
-  NFS_CUDA(nfs::launch_prep_tables(d_temp, nullptr, K, 0, p1, nt, d_tt, nullptr, P->stream));
+  NFS_CUDA(nfs::launch_prep_tables(d_temp, nullptr, K, 0, p1, nt, d_tt, nullptr, P->stream, false,
+                                   P->prec == NFS_PREC_FP64));
   NFS_CUDA(nfs::launch_spatial_from_grid(d_vox, d_b0, L, nt, dims, fov, order, d_rr, P->stream));
   return finish_tables(P, d_tt, d_rr);
 }
