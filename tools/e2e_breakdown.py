@@ -1,29 +1,60 @@
-"""Wall-clock breakdown of one recon_full on config B (plan, uploads, CG, finalize)."""
-import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+"""Where the end-to-end time of a recon_full goes (config B by default).
+
+    python tools/e2e_breakdown.py [--config B] [--precision f16x3] [--reps 3]
+
+Prints the CGLog timing labels of `engine.recon_full` (plan + table upload, S' upload, samples
+upload, initial adjoint, per-iteration device times) next to the wall time of the whole call,
+so the part of the e2e number that is not E^H E applies is visible.
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
 import numpy as np
-from paper_2604_09233_b200 import engine, simulate
-prec = os.environ.get("PREC", "f16x3")
-from paper_2604_09233_b200._native import Plan
-prob = simulate.make_problem("B")
-K, L, G = prob.temporal.shape[0], prob.spatial.shape[1], prob.sens.shape[1]
-pl = Plan(K, L, G, prob.spatial.shape[0], "fp32"); pl.set_tables(prob.temporal, prob.spatial)
-pl.set_sens(prob.sens, prob.intensity); sig = pl.apply_E(prob.rho_true / prob.intensity); pl.close()
-for rep in range(2):
-    inputs = engine.EncodingInputs(sigma=sig, spatial=prob.spatial,
-                                   temporal=prob.temporal, sens=prob.sens, intensity=prob.intensity,
-                                   kfilter=None, mask_r=prob.mask_r, grid=prob.grid, n_iter=20)
-    t0 = time.perf_counter()
-    img, log = engine.recon_full(inputs, precision=prec)
-    wall = time.perf_counter() - t0
-    tim = dict(log.timings) if hasattr(log, "timings") else {}
-    cg = sum(v for k, v in tim.items() if k.startswith("cg_iteration"))
-    print(f"rep {rep}: wall {wall*1e3:.1f} ms | " + " ".join(f"{k}={v*1e3:.1f}" for k, v in tim.items()
-          if not k.startswith("cg_iteration")) + f" cg_total={cg*1e3:.1f}")
-for rep in range(3):
-    t0 = time.perf_counter(); p = Plan(K, L, G, prob.spatial.shape[0], prec); t1 = time.perf_counter()
-    p.set_sens(prob.sens, prob.intensity); t2 = time.perf_counter()
-    p.set_tables(prob.temporal, prob.spatial); t3 = time.perf_counter()
-    p.set_samples(sig); t4 = time.perf_counter()
-    p.close(); t5 = time.perf_counter()
-    print(f"plan {1e3*(t1-t0):.1f} sens {1e3*(t2-t1):.1f} tables {1e3*(t3-t2):.1f} samples {1e3*(t4-t3):.1f} close {1e3*(t5-t4):.1f} ms")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="B")
+    ap.add_argument("--precision", default="f16x3")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--iters", type=int, default=20)
+    args = ap.parse_args()
+    import torch
+    from paper_2604_09233_b200 import _native, engine, simulate
+
+    prob = simulate.make_problem(args.config)
+    K, L = prob.temporal.shape[0], prob.spatial.shape[1]
+    plan = _native.Plan(K, L, prob.sens.shape[1], prob.spatial.shape[0], args.precision)
+    plan.set_tables(prob.temporal, prob.spatial)
+    plan.set_sens(prob.sens, prob.intensity)
+    sigma = plan.apply_E(prob.rho_true / prob.intensity)
+    plan.close()
+    inputs = engine.EncodingInputs(sigma=sigma, spatial=prob.spatial, temporal=prob.temporal, sens=prob.sens,
+                                   intensity=prob.intensity, kfilter=None, mask_r=prob.mask_r, grid=prob.grid,
+                                   n_iter=args.iters)
+    out = []
+    for _ in range(args.reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        img, log = engine.recon_full(inputs, precision=args.precision)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        tim = dict(log.timings)
+        it = [v for k, v in log.timings if k.startswith("cg_iteration_")]
+        rec = {"wall_s": wall, "iterations_s": float(np.sum(it)), "iteration_mean_ms": 1e3 * float(np.mean(it)),
+               **{k: v for k, v in tim.items() if not k.startswith("cg_iteration_")}}
+        rec["unlabelled_s"] = wall - sum(v for k, v in tim.items() if not k.startswith("cg_iteration_")) \
+            - rec["iterations_s"]
+        out.append(rec)
+        print(json.dumps(rec), flush=True)
+
+
+if __name__ == "__main__":
+    main()
