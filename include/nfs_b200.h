@@ -73,16 +73,6 @@ int nfs_comm_create(const void* nccl_unique_id, int32_t rank, int32_t world, int
 void nfs_comm_destroy(void* comm);
 int nfs_plan_use_comm(nfs_plan* plan, void* comm, int32_t rank, int32_t world);
 
-/* Resident phase (NFS_PREC_F16X3 only; call after the tables).  mode 1 computes the exact
- * 32-bit phase of every (sample, voxel) pair ONCE -- one pass of the int8 phase MMA -- and keeps
- * it in HBM (8 bytes per pair: one copy in each operator's tiling), so every following E / E^H
- * streams it instead of regenerating it: the analogue of the reference's recon_full, which
- * builds the phase matrix once and keeps it (nfs/engine.py:125-148).  Results are bit-identical
- * to the on-the-fly operators; nfs_set_tables rebuilds it.  mode 0 frees it; mode -1 only
- * reports.  bytes_out (optional) = the HBM it takes.  NFS_ERR_BUDGET when the device memory
- * is not available (the plan stays on the fly). */
-int nfs_plan_set_phase_resident(nfs_plan* plan, int32_t mode, int64_t* bytes_out);
-
 /* Basis tables: temporal rows of this rank (K x P1) and spatial (P1 x L_R). */
 int nfs_set_tables(nfs_plan* plan, const double* temporal, const double* spatial);
 /* Same, with the spatial table voxel-major (L_R x P1): the memory of the Fortran-ordered

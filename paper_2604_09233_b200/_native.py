@@ -40,7 +40,6 @@ SIGNATURES = {
     "nfs_comm_create": (_c_i32, [ctypes.c_char_p, _c_i32, _c_i32, _c_i32, ctypes.POINTER(_c_void_p)]),
     "nfs_comm_destroy": (None, [_c_void_p]),
     "nfs_plan_use_comm": (_c_i32, [_c_void_p, _c_void_p, _c_i32, _c_i32]),
-    "nfs_plan_set_phase_resident": (_c_i32, [_c_void_p, _c_i32, ctypes.POINTER(_c_i64)]),
     "nfs_set_tables": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
     "nfs_set_tables_t": (_c_i32, [_c_void_p, _c_dbl_p, _c_dbl_p]),
     "nfs_set_tables_grid": (_c_i32, [_c_void_p, _c_dbl_p, ctypes.POINTER(_c_i64), _c_dbl_p,
@@ -157,13 +156,6 @@ class Plan:
 
     def use_comm(self, comm: "SharedComm"):
         _check(self._lib.nfs_plan_use_comm(self._h, comm.handle, comm.rank, comm.world))
-
-    def set_phase_resident(self, mode: int = 1) -> int:
-        """f16x3 only: 1 = build the resident phase (after the tables), 0 = free it, -1 = query.
-        Returns the HBM bytes it takes; raises MemoryBudgetError when it does not fit."""
-        nbytes = _c_i64(0)
-        _check(self._lib.nfs_plan_set_phase_resident(self._h, int(mode), ctypes.byref(nbytes)))
-        return int(nbytes.value)
 
     # -- inputs ------------------------------------------------------------------
     def set_tables(self, temporal, spatial):

@@ -1120,26 +1120,3 @@ extern "C" int nfs_launches_per_apply(nfs_plan* P) {
 }
 
 extern "C" const char* nfs_plan_describe(nfs_plan* P) { return P ? P->desc.c_str() : ""; }
-
-extern "C" int nfs_debug_resident_copy(nfs_plan* P, int32_t fwd, void* dst, int64_t bytes) {   // debugging only
-  return P && P->tci ? nfs::tci_debug_resident(P->tci, fwd, dst, (size_t)bytes) : 1;
-}
-
-// Resident phase of the f16x3 operator (the analogue of recon_full's phase matrix kept in
-// memory, nfs/engine.py:125-148): mode 1 builds it (needs the tables), 0 frees it, -1 only
-// reports the bytes it takes.
-extern "C" int nfs_plan_set_phase_resident(nfs_plan* P, int32_t mode, int64_t* bytes_out) {
-  if (!P) return fail(NFS_ERR_INVALID, "null plan");
-  if (!P->tci) return fail(NFS_ERR_INVALID, "the resident phase needs the f16x3 tensor-core operator");
-  if (bytes_out) *bytes_out = (int64_t)nfs::tci_resident_bytes(P->tci);
-  if (mode < 0) return NFS_OK;
-  const int s = nfs::tci_set_resident(P->tci, mode != 0, P->stream);
-  if (s == 3) return fail(NFS_ERR_BUDGET, nfs::tci_last_error());
-  if (s) return fail(NFS_ERR_INVALID, nfs::tci_last_error());
-  NFS_CUDA(cudaStreamSynchronize(P->stream));
-  const std::string tag = " [resident phase]";
-  const size_t at = P->desc.find(tag);
-  if (mode != 0 && at == std::string::npos) P->desc += tag;
-  if (mode == 0 && at != std::string::npos) P->desc.erase(at, tag.size());
-  return NFS_OK;
-}

@@ -23,13 +23,6 @@ int tci_set_sens(TciPlan* t, const void* d_S, int ldc, cudaStream_t st);
 int tci_forward_parts(TciPlan* t, const double2* p, void* y, const int* stop, cudaStream_t st, int part);
 int tci_adjoint_parts(TciPlan* t, const void* y, double2* q, const int* stop, cudaStream_t st, int part);
 int tci_launches_per_apply(TciPlan* t);
-// resident phase: build (on = true) or drop the exact 32-bit phase of every (sample, voxel) pair
-// in HBM (two copies, 8 bytes per pair); the operators then stream it instead of recomputing
-// it.  Returns 3 when the device memory is not available (the plan stays on the fly).
-int tci_set_resident(TciPlan* t, bool on, cudaStream_t st);
-size_t tci_resident_bytes(TciPlan* t);
-bool tci_is_resident(TciPlan* t);
-int tci_debug_resident(TciPlan* t, int fwd, void* dst, size_t bytes);
 int tci_coil_width(int G);
 
 }  // namespace nfs
