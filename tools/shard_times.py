@@ -49,7 +49,8 @@ def main():
         base = worst if world == 1 else base
         print(json.dumps({"config": args.config, "world": world, "rows_per_rank": [r[1] - r[0] for r in (ranks[0], ranks[-1])],
                           "apply_ms_slowest_rank": worst, "kernel_ms_fwd_adj": kern[-1],
-                          "efficiency_before_allreduce": base / (world * worst), "plan": desc}), flush=True)
+                          "efficiency_before_allreduce": base / (world * worst) if base else None,
+                          "plan": desc}), flush=True)
 
 
 if __name__ == "__main__":
