@@ -91,6 +91,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     if (done) break;
   }
 }
+#ifndef NFS_TC_JITTER
+#define NFS_TC_JITTER 0
+#endif
+// Race-detection builds only (tests/test_gpu_race_jitter.py, -DNFS_TC_JITTER=1): pseudo-random
+// sleeps of up to ~2 us at one in four hand-offs of every warp role; compiled out otherwise.
+__device__ __forceinline__ void jitter(uint32_t key) {
+#if NFS_TC_JITTER
+  uint32_t h = key * 2654435761u ^ (blockIdx.x * 40503u + blockIdx.y * 977u + 0x9e3779b9u);
+  h ^= h >> 15;
+  h *= 2246822519u;
+  h ^= h >> 13;
+  if ((h & 3u) == 0u) __nanosleep(h >> 21);
+#else
+  (void)key;
+#endif
+}
+
 // wait for a single-thread role (producer, MMA issuer, drain): let the hardware suspend the
 // warp instead of spinning, so it does not steal issue slots from the generator warps
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
@@ -309,6 +326,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
     // TMEM D buffer of segment d -> smem accumulator (FP32 round-to-nearest adds)
     auto drain = [&](int d) {
       const int db = d & 1;
+      jitter((uint32_t)d * 64u + 60u + (uint32_t)q);
       mbar_wait_sleep(&dfull[db], (d >> 1) & 1);
       fence_after();
 #pragma unroll
@@ -327,6 +345,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
     // warp (q, h) owns chunks c = h, h + GPQ, ... for its lane quadrant: the warps of a
     // quadrant work on different chunks, so their barrier waits do not line up
     for (int c = h; c < n_chunks; c += GPQ) {
+      jitter((uint32_t)c * 64u + (uint32_t)warp);
       const int sb = c % SB, sa = c % SA;
       mbar_wait(&full_b[sb], (c / SB) & 1);
       const float* tb = sT + sb * (T_STAGE_BYTES / 4);
@@ -415,6 +434,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
       for (int c = 0; c < n_chunks; ++c) {
         const int sb = c % SB;
         mbar_wait_sleep(&empty_a[sb], ((c / SB) & 1) ^ 1);
+        jitter((uint32_t)c * 64u + 50u);
         const int gc = chunk0 + c;
         if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && c < 64) a.trace[c * 4 + 0] = clock64();
         if (TC_DEBUG & 8) { mbar_arrive(&full_b[sb]); continue; }
@@ -435,6 +455,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) tc_contract_kernel(Args 
       constexpr int COLS_PER_STEP = K_::kstep * K_::ebytes / 4;
       for (int c = 0; c < n_chunks; ++c) {
         const int sb = c % SB, sa = c % SA, seg = c / SEG, db = seg & 1;
+        jitter((uint32_t)c * 64u + 41u);
         if (c % SEG == 0) {
           mbar_wait_sleep(&dempty[db], ((seg >> 1) & 1) ^ 1);   // segment seg-2 drained from buffer db
           fence_after();

@@ -1,4 +1,4 @@
-"""A/B helper: one f16x3 apply_E / apply_EH / 5-iteration CG of a config through the library in
+"""A/B helper: one apply_E / apply_EH / 5-iteration CG of a config through the library in
 NFS_B200_LIB, saved to an .npz, so two builds can be compared bit for bit.
 
     NFS_B200_LIB=tools/variants/lib_x.so python tools/ab_check.py --config B --out gpurun_out/ab_x.npz
@@ -15,6 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="B")
 ap.add_argument("--scale", type=int, default=1)
+ap.add_argument("--precision", default="f16x3")
 ap.add_argument("--out")
 ap.add_argument("--compare", nargs=2)
 a = ap.parse_args()
@@ -29,7 +30,7 @@ from paper_2604_09233_b200 import _native, simulate  # noqa: E402
 
 prob = simulate.make_problem(a.config, scale=a.scale)
 K, L = prob.temporal.shape[0], prob.spatial.shape[1]
-plan = _native.Plan(K, L, prob.sens.shape[1], prob.spatial.shape[0], "f16x3", 0)
+plan = _native.Plan(K, L, prob.sens.shape[1], prob.spatial.shape[0], a.precision, 0)
 plan.set_tables(prob.temporal, prob.spatial)
 plan.set_sens(prob.sens, prob.intensity)
 rng = np.random.default_rng(11)
