@@ -18,3 +18,8 @@ for c in range(24):
     print(c, *a[c][:6], '|', *a[c][6:10], '|', *a[c][10:12])
 d = np.diff(a[4:60, 4])
 print("mean cycles per chunk (issuer start to start):", d.mean())
+b = np.ctypeslib.as_array(tr, shape=(64 * 12 + 64 * 8,)).copy()[768:].reshape(64, 8)
+b = np.where(b > 0, b - np.ctypeslib.as_array(tr, shape=(768,))[0], 0)
+print("per-quadrant: chunk | phase got q0..q3 | phase released q0..q3 | next phIssued")
+for c in range(4, 24):
+    print(c, *b[c][4:], '|', *b[c][:4], '|', a[c + 4][0] if c + 4 < 64 else '')
