@@ -233,9 +233,11 @@ def config_a_sigma(prob):
 
 
 def cpu_sample_rows(cfg):
-    # ~10 s of CPU work per sample on an 8-32 core host: np.exp dominates (single-threaded,
-    # ~35-57 ns per element)
-    return {"B": 3 * 402, "C": 3 * 402, "D": 256}[cfg]
+    # a bounded sample of the workload: whole 2^28-byte phase blocks of the reference's
+    # recon_split (402 rows each at config B/C), ~5-9 s of CPU work per sample on the 16-core GPU
+    # host (np.exp dominates, single-threaded: SURVEY Appendix B), so the cpu_baseline leg (two
+    # samples) takes ~10-20 s and a 20-step reference arm a few minutes
+    return {"B": 15 * 402, "C": 15 * 402, "D": 512}[cfg]
 
 
 def run_reference_arm(args):
