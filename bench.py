@@ -234,10 +234,11 @@ def config_a_sigma(prob):
 
 def cpu_sample_rows(cfg):
     # a bounded sample of the workload: whole 2^28-byte phase blocks of the reference's
-    # recon_split (402 rows each at config B/C), ~5-9 s of CPU work per sample on the 16-core GPU
-    # host (np.exp dominates, single-threaded: SURVEY Appendix B), so the cpu_baseline leg (two
-    # samples) takes ~10-20 s and a 20-step reference arm a few minutes
-    return {"B": 15 * 402, "C": 15 * 402, "D": 512}[cfg]
+    # recon_split (402 rows each at config B/C), ~4 s of timed CPU E^H E per sample on the
+    # 16-core GPU host (~7 s of wall time with the sample's initial adjoint; np.exp dominates,
+    # single-threaded: SURVEY Appendix B), so the cpu_baseline leg (two samples) takes ~15 s and a
+    # 20-step reference arm ~2.5 minutes
+    return {"B": 10 * 402, "C": 10 * 402, "D": 256}[cfg]
 
 
 def run_reference_arm(args):
