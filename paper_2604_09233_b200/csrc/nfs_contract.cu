@@ -232,8 +232,14 @@ __global__ void __launch_bounds__(kBlockF) contract_f32_kernel(ContractLaunch a)
 
 // ------------------------------------------------------------------ FP64 scalar kernel
 __host__ __device__ constexpr int ro_f64(int nc, int nt) { return nc >= 16 ? 1 : (nt >= 20 ? 1 : 2); }
-constexpr int kBlockD = 128;
-constexpr int kChunkD = 32;
+#ifndef NFS_F64_BLOCK
+#define NFS_F64_BLOCK 128   // 256: 2-5% faster at config B, but it changes config D's split and its chaotic 50-iteration drift (DESIGN 3.2)
+#endif
+#ifndef NFS_F64_CHUNK
+#define NFS_F64_CHUNK 32
+#endif
+constexpr int kBlockD = NFS_F64_BLOCK;
+constexpr int kChunkD = NFS_F64_CHUNK;
 
 template <int NC, int NT, bool FWD>
 __global__ void __launch_bounds__(kBlockD) contract_f64_kernel(ContractLaunch a) {
